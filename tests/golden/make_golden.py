@@ -1,0 +1,296 @@
+"""Generate the golden PHG fixtures by running the REFERENCE implementation.
+
+Run in the build container only (it imports strandkit from /root/reference,
+which does not exist on the GPU box):
+
+    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py
+
+Every fixture is one compressed .npz holding the exact inputs (field bytes,
+seeds, params, cap / near-occupancy / counts planes) and the reference's
+outputs in CSR form (offsets (n+1,), verts (M,3) f64, entered (n,)).  The
+oracle (oracle/) is pinned bit-exact against these; the CUDA path is checked
+against them in tests/test_gpu_parity.py.
+
+Reference entry points exercised:
+  strandkit.phg.trace_batch                 phg.py:67-163
+  strandkit.volume.sample_orientation_batch volume.py:183-224
+  strandkit.phg.init_guide_strands          phg.py:210-260 (incl. _trace_field_seeds :263-303)
+  strandkit.phg.nearest_occupied_map        phg.py:57-64 (steer input)
+Unit cases restate the inputs of the reference's own trace tests
+(pkg/tests/test_phg.py:33-127, test_acceptance.py:224-262).
+"""
+
+import json
+import os
+import sys
+
+import numpy as np
+
+sys.dont_write_bytecode = True
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, "/root/reference/pkg/src")
+sys.path.insert(0, ROOT)
+
+from strandkit import phg  # noqa: E402
+from strandkit.scalp import ScalpMesh  # noqa: E402
+from strandkit.volume import OOVolume, sample_orientation_batch  # noqa: E402
+
+from paper_2604_05794_b200 import synth  # noqa: E402
+
+TRACE_KEYS = ("step_mm", "max_vertices", "min_support", "probe_steps", "coast_steps", "steer",
+              "strict", "occupancy_cap", "batch_size", "field_seeds")
+
+
+def params_json(p):
+    return json.dumps({k: getattr(p, k) for k in TRACE_KEYS})
+
+
+def to_csr(out):
+    lens = np.array([len(v) for v, _ in out], dtype=np.int64)
+    offsets = np.zeros(len(out) + 1, dtype=np.int64)
+    np.cumsum(lens, out=offsets[1:])
+    verts = np.concatenate([v for v, _ in out]) if out else np.zeros((0, 3))
+    entered = np.array([e for _, e in out], dtype=bool)
+    return offsets, verts, entered
+
+
+def vol_of(origin, vs, occ, ori):
+    vol = OOVolume.empty(origin, vs, occ.shape)
+    vol.occ = occ.copy()
+    vol.ori = ori.astype(np.float32).copy()
+    return vol
+
+
+def save(name, vol, seeds, dirs, params, out, at_cap=None, near_occ=None, counts_in=None,
+         counts_out=None, extra=None):
+    offsets, verts, entered = to_csr(out)
+    d = dict(
+        origin=np.asarray(vol.origin, np.float64), voxel_size=np.float64(vol.voxel_size),
+        occ=vol.occ, ori=vol.ori, seeds=np.asarray(seeds, np.float64).reshape(-1, 3),
+        dirs=np.asarray(dirs, np.float64).reshape(-1, 3), params=np.array(params_json(params)),
+        offsets=offsets, verts=verts, entered=entered,
+    )
+    if at_cap is not None:
+        d["at_cap"] = at_cap
+    if near_occ is not None:
+        d["near_occ"] = near_occ.astype(np.int64)
+    if counts_in is not None:
+        d["counts_in"] = counts_in
+    if counts_out is not None:
+        d["counts_out"] = counts_out
+    if extra:
+        d.update(extra)
+    path = os.path.join(HERE, f"trace_{name}.npz")
+    np.savez_compressed(path, **d)
+    steps = int((np.diff(offsets) - 1).sum()) if len(out) else 0
+    print(f"{name:24s} n={len(out):5d} M={len(verts):7d} steps={steps:7d} "
+          f"{os.path.getsize(path) / 1e3:8.1f} kB")
+
+
+def column(height=40, ori=(0.0, 0.0, 1.0)):
+    """The reference tests' column volume (test_phg.py:14-19)."""
+    vol = OOVolume.empty(origin=(-10.0, -10.0, 0.0), voxel_size=2.0, dims=(10, 10, height))
+    vol.occ[:] = True
+    vol.ori[:] = np.asarray(ori, dtype=np.float32)
+    return vol
+
+
+def unit_cases():
+    P = phg.PhgParams
+    up = [[0.0, 0.0, 1.0]]
+    s0 = [[0.5, 0.5, 1.0]]
+    vol = column()
+    p = P(step_mm=1.0, max_vertices=30, probe_steps=0, coast_steps=0, field_seeds=0)
+    save("unit_straight", vol, s0, up, p, phg.trace_batch(vol, s0, up, p))
+    vol = column(height=5)
+    p = P(step_mm=1.0, max_vertices=60, probe_steps=0, coast_steps=0, field_seeds=0)
+    save("unit_slab_top", vol, s0, up, p, phg.trace_batch(vol, s0, up, p))
+    for steps in (2, 15):
+        vol = column()
+        vol.occ[:, :, :6] = False
+        p = P(step_mm=1.0, max_vertices=40, probe_steps=steps, coast_steps=0, field_seeds=0)
+        save(f"unit_probe{steps}", vol, s0, up, p, phg.trace_batch(vol, s0, up, p))
+    for coast in (0, 12):
+        vol = column()
+        vol.occ[:, :, 10:13] = False
+        p = P(step_mm=1.0, max_vertices=90, probe_steps=0, field_seeds=0, coast_steps=coast)
+        save(f"unit_coast{coast}", vol, s0, up, p, phg.trace_batch(vol, s0, up, p))
+    vol = column(height=10)
+    p = P(step_mm=1.0, max_vertices=80, probe_steps=0, coast_steps=10, field_seeds=0)
+    save("unit_trim", vol, s0, up, p, phg.trace_batch(vol, s0, up, p))
+    vol = column()
+    p = P(step_mm=1.0, max_vertices=30, probe_steps=0, coast_steps=0, field_seeds=0, strict=True)
+    seeds = np.array([[0.5, 0.5, 1.0], [0.5, 0.5, 0.2]])
+    dirs = np.array([[0.0, 0.0, 1.0], [0.0, 0.0, 1.0]])
+    counts = np.zeros(vol.dims, np.uint16)
+    c0 = counts.copy()
+    out = phg.trace_batch(vol, seeds, dirs, p, live_counts=counts)
+    save("unit_strict", vol, seeds, dirs, p, out, counts_in=c0, counts_out=counts)
+    vol = column()
+    p = P(step_mm=1.0, max_vertices=30, probe_steps=0, coast_steps=0, field_seeds=0,
+          occupancy_cap=1)
+    seeds = np.tile([[0.5, 0.5, 1.0]], (4, 1))
+    dirs = np.tile([[0.0, 0.0, 1.0]], (4, 1))
+    cap = np.zeros(vol.dims, dtype=bool)
+    save("unit_deferred", vol, seeds, dirs, p, phg.trace_batch(vol, seeds, dirs, p, at_cap=cap),
+         at_cap=cap)
+    vol = column()
+    p = P(step_mm=1.0, max_vertices=30, probe_steps=0, coast_steps=0, field_seeds=0)
+    cap = np.zeros(vol.dims, dtype=bool)
+    cap[:, :, 8:] = True
+    save("unit_at_cap", vol, s0, up, p, phg.trace_batch(vol, s0, up, p, at_cap=cap), at_cap=cap)
+    # max_vertices edge cases and a seed far outside the volume
+    vol = column()
+    for mv in (1, 2):
+        p = P(max_vertices=mv, field_seeds=0)
+        save(f"unit_maxv{mv}", vol, s0 + [[100.0, 0, 0]], up + up, p,
+             phg.trace_batch(vol, s0 + [[100.0, 0, 0]], up + up, p))
+    seeds = np.array([[500.0, 500.0, 500.0], [-3.0, 2.0, -30.0], [0.5, 0.5, 79.9], [0.0, 0.0, 40.0]])
+    dirs = np.array([[0.0, 0.0, 1.0], [0.0, 0.0, 1.0], [0.0, 0.0, 1.0], [1e-14, 0.0, 0.0]])
+    p = P(field_seeds=0)
+    save("unit_outside", vol, seeds, dirs, p, phg.trace_batch(vol, seeds, dirs, p))
+    # zero seeds
+    p = P(field_seeds=0)
+    save("unit_empty", vol, np.zeros((0, 3)), np.zeros((0, 3)), p,
+         phg.trace_batch(vol, np.zeros((0, 3)), np.zeros((0, 3)), p))
+
+
+def helix_case():
+    """A8 helix field (test_acceptance.py:224-262), nearest-helix-point orientation."""
+    from scipy.spatial import cKDTree
+
+    r, pitch, vs = 20.0, 40.0, 2.0
+    b = pitch / (2 * np.pi)
+    speed = np.hypot(r, b)
+
+    def helix(t):
+        return np.stack([r * np.cos(t), r * np.sin(t), b * t], axis=-1)
+
+    def helix_tan(t):
+        v = np.stack([-r * np.sin(t), r * np.cos(t), np.full_like(t, b)], axis=-1)
+        return v / np.linalg.norm(v, axis=-1, keepdims=True)
+
+    tmax = 180.0 / speed
+    origin = np.array([-r - 10.0, -r - 10.0, -10.0])
+    dims = (int((2 * r + 20) / vs) + 1, int((2 * r + 20) / vs) + 1, int((b * tmax + 20) / vs) + 1)
+    vol = OOVolume.empty(origin, vs, dims)
+    grid = np.stack(np.meshgrid(*[np.arange(d) for d in dims], indexing="ij"), axis=-1).reshape(-1, 3)
+    centers = vol.centers(grid)
+    ts = np.linspace(0, tmax, 4000)
+    d, i = cKDTree(helix(ts)).query(centers)
+    occ = d < 6.0
+    vol.occ = occ.reshape(dims)
+    ori = np.zeros((len(centers), 3))
+    ori[occ] = helix_tan(ts[i[occ]])
+    vol.ori = ori.reshape(*dims, 3).astype(np.float32)
+    p = phg.PhgParams(step_mm=1.0, max_vertices=101, probe_steps=0, coast_steps=0, field_seeds=0)
+    ts0 = np.linspace(0.2, 0.6, 40)
+    seeds, dirs = helix(ts0), helix_tan(ts0)
+    save("helix", vol, seeds, dirs, p, phg.trace_batch(vol, seeds, dirs, p))
+
+
+def field_np(kind, n, **kw):
+    ori, occ = synth.make_field(kind, n, "cpu", **kw)
+    return ori.numpy(), occ.numpy()
+
+
+def analytic_cases():
+    P = phg.PhgParams
+    for kind, n, count, key in (("straight", 48, 600, 21), ("wavy", 48, 600, 22),
+                                ("curly", 48, 150, 23)):
+        ori, occ = field_np(kind, n)
+        vol = vol_of((0, 0, 0), synth.VOXEL_MM, occ, ori)
+        seeds, dirs = synth.disk_seeds(n, count, key)
+        p = P(field_seeds=0, batch_size=count)
+        save(f"{kind}{n}", vol, seeds, dirs, p,
+             phg.trace_batch(vol, seeds, dirs, p, at_cap=np.zeros(occ.shape, bool)))
+    # sparse field: scalp seeds + interior seeds in both directions
+    n = 48
+    ori, occ = field_np("sparse", n, sparse_sigma=2.0)
+    vol = vol_of((0, 0, 0), synth.VOXEL_MM, occ, ori)
+    s1, d1 = synth.disk_seeds(n, 400, 24, radius_frac=0.45)
+    s2, d2 = synth.interior_seeds(occ, ori, 400, 25)
+    seeds = np.concatenate([s1, s2, s2])
+    dirs = np.concatenate([d1, d2, -d2])
+    p = P(field_seeds=0)
+    save("sparse48", vol, seeds, dirs, p, phg.trace_batch(vol, seeds, dirs, p))
+    # non-empty cap plane on the curly field (caps must be covered)
+    ori, occ = field_np("curly", 40)
+    vol = vol_of((0, 0, 0), synth.VOXEL_MM, occ, ori)
+    rng = np.random.Generator(np.random.Philox(key=26))
+    cap = rng.random(occ.shape) < 0.04
+    seeds, dirs = synth.disk_seeds(40, 500, 27)
+    p = P(field_seeds=0, probe_steps=5, coast_steps=3)
+    save("curly40_cap", vol, seeds, dirs, p, phg.trace_batch(vol, seeds, dirs, p, at_cap=cap),
+         at_cap=cap)
+    # non power-of-two voxel size and a shifted origin
+    ori, occ = field_np("curly", 32)
+    vol = vol_of((-31.7, 12.25, -3.0), 1.7, occ, ori)
+    s, d = synth.disk_seeds(32, 100, 28)
+    s = (s / synth.VOXEL_MM) * 1.7 + vol.origin
+    p = P(field_seeds=0, step_mm=0.85, min_support=0.2)
+    save("curly32_vs17", vol, s, d, p, phg.trace_batch(vol, s, d, p))
+    # steer: sparse field, coasting strands pulled toward occupied voxels
+    ori, occ = field_np("sparse", 40, sparse_sigma=2.0, sparse_key=9)
+    vol = vol_of((0, 0, 0), synth.VOXEL_MM, occ, ori)
+    near = phg.nearest_occupied_map(vol)
+    s1, d1 = synth.disk_seeds(40, 300, 29, radius_frac=0.45)
+    s2, d2 = synth.interior_seeds(occ, ori, 200, 30)
+    seeds, dirs = np.concatenate([s1, s2]), np.concatenate([d1, d2])
+    p = P(field_seeds=0, steer=0.5, coast_steps=8)
+    save("sparse40_steer", vol, seeds, dirs, p,
+         phg.trace_batch(vol, seeds, dirs, p, near_occ=near), near_occ=near)
+    # strict mode with many interacting strands
+    ori, occ = field_np("curly", 32)
+    vol = vol_of((0, 0, 0), synth.VOXEL_MM, occ, ori)
+    seeds, dirs = synth.disk_seeds(32, 300, 31)
+    counts = np.zeros(occ.shape, np.uint16)
+    counts[rng.random(occ.shape) < 0.01] = 1
+    c0 = counts.copy()
+    p = P(field_seeds=0, strict=True)
+    out = phg.trace_batch(vol, seeds, dirs, p, live_counts=counts)
+    save("curly32_strict", vol, seeds, dirs, p, out, counts_in=c0, counts_out=counts)
+
+
+def sampler_case():
+    ori, occ = field_np("sparse", 24, sparse_sigma=1.5)
+    vol = vol_of((-5.0, 3.0, 1.0), 1.5, occ, ori)
+    rng = np.random.Generator(np.random.Philox(key=33))
+    lo, hi = vol.origin - 3.0, vol.origin + np.array(vol.dims) * 1.5 + 3.0
+    pts = rng.uniform(lo, hi, size=(4000, 3))
+    prev = rng.normal(size=(4000, 3))
+    prev /= np.linalg.norm(prev, axis=1, keepdims=True)
+    dirs, has, sup = sample_orientation_batch(vol, pts, prev)
+    np.savez_compressed(os.path.join(HERE, "sample_sparse24.npz"), origin=vol.origin,
+                        voxel_size=np.float64(vol.voxel_size), occ=vol.occ, ori=vol.ori, pts=pts,
+                        prev=prev, dirs=dirs, has=has, support=sup)
+    print("sample_sparse24 ok")
+
+
+def driver_case():
+    """init_guide_strands with several deferred-commit batches and a field pass."""
+    n = 40
+    ori, occ = field_np("sparse", n, sparse_sigma=2.0, sparse_key=7)
+    vol = vol_of((0, 0, 0), synth.VOXEL_MM, occ, ori)
+    seeds, dirs = synth.disk_seeds(n, 1500, 34, radius_frac=0.45)
+    scalp = ScalpMesh(vertices=np.zeros((3, 3)), faces=np.zeros((1, 3), int),
+                      vertex_normals=np.zeros((3, 3)), seeds=seeds, seed_normals=dirs)
+    p = phg.PhgParams(batch_size=256, occupancy_cap=2, field_seeds=600, n_root=1500)
+    segs, report = phg.init_guide_strands(scalp, vol, p, workers=1)
+    out = [(s.vertices, s.rooted) for s in segs]
+    offsets, verts, rooted = to_csr(out)
+    np.savez_compressed(
+        os.path.join(HERE, "driver_sparse40.npz"), origin=vol.origin,
+        voxel_size=np.float64(vol.voxel_size), occ=vol.occ, ori=vol.ori, seeds=seeds, dirs=dirs,
+        params=np.array(params_json(p)), offsets=offsets, verts=verts, rooted=rooted,
+        counts_out=vol.counts, report=np.array(json.dumps(report)))
+    print(f"driver_sparse40 segments={len(segs)} report={report}")
+
+
+if __name__ == "__main__":
+    unit_cases()
+    helix_case()
+    analytic_cases()
+    sampler_case()
+    driver_case()
