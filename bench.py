@@ -1,0 +1,386 @@
+"""PHG strand-vertex steps/s on B200 (BASELINE.json metric; workload C3 by default).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C3]
+
+One step = one trace of this rank's seed batch: every seed
+integrated to termination through the field, kept vertices scanned and
+gathered into the CSR payload (K1 + K2), plus -- at N > 1 -- the final
+all-gather of per-rank (strands, vertices) that yields global CSR offsets.
+Steps are counted as the reference counts them: sum over returned strands of
+(len(vertices) - 1).
+
+Multi-GPU: one process per GPU (torchrun), field replicated, seeds of the
+global batch partitioned in contiguous rank slices, per-GPU seed count fixed
+("weak" scaling).  Rank 0 prints one JSON line.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+BYTES_PER_STEP = 2 * 8 * 16 + 1 + 24  # 2 samples x 8 float4 corners + cap probe + f64 vertex
+METRIC = "PHG strand-vertex steps/sec at 1/2/4/8 B200 (512³ field, 1M seeds)"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C3")
+    ap.add_argument("--seeds", type=int, default=0, help="override seeds per rank")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-sample", type=int, default=0, help="seeds in the CPU sample")
+    return ap.parse_args()
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def measured_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:  # noqa: BLE001
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic():
+    """Per-launch DRAM bytes of the trace kernel from the committed ncu summary, if any."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_trace_summary.json")) as f:
+            d = json.load(f)
+        return d.get("dram_bytes_per_launch"), d.get("steps_per_launch")
+    except Exception:  # noqa: BLE001
+        return None, None
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:  # noqa: BLE001
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return None
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:  # noqa: BLE001
+            self.proc.kill()
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower() in ("active", "1", "yes"):
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_host_info():
+    cores = len(os.sched_getaffinity(0))
+    model = ""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except Exception:  # noqa: BLE001
+        pass
+    return cores, model
+
+
+def cpu_numpy_port(ori, occ, seeds, dirs, params, workers):
+    """The reference's algorithm as the reference runs it (numpy, fork pool) -- oracle port."""
+    from oracle import phg_oracle_np as onp  # CPU baseline leg only
+
+    f = onp.Field(np.zeros(3), 2.0, occ.shape, occ, ori)
+    t0 = time.perf_counter()
+    steps = onp.steps_multicore(f, seeds, dirs, params, workers=workers)
+    return steps, time.perf_counter() - t0
+
+
+def cpu_c_port(ori, occ, seeds, dirs, params, threads):
+    from oracle import phg_oracle_c as oc  # CPU baseline leg only
+
+    t0 = time.perf_counter()
+    _, keep, _ = oc.trace(np.zeros(3), 2.0, occ, ori, seeds, dirs, params, threads=threads)
+    return int((keep - 1).sum()), time.perf_counter() - t0
+
+
+def host_field(cfg):
+    from paper_2604_05794_b200 import synth
+
+    ori, occ = synth.make_field(cfg.kind, cfg.n, "cpu")
+    return ori.numpy(), occ.numpy()
+
+
+def run_reference(args):
+    """--impl reference: the reference CPU path (numpy port, all host cores) on rank 0 only."""
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    from paper_2604_05794_b200 import synth
+    from paper_2604_05794_b200.phg import PhgParams
+
+    cfg = synth.CONFIGS[args.config]
+    cores, model = cpu_host_info()
+    params = PhgParams(field_seeds=0)
+    ori, occ = host_field(cfg)
+    sample = args.cpu_sample or max(1024, cores * 256)
+    seeds, dirs = synth.disk_seeds(cfg.n, cfg.seeds * max(ws, 1), cfg.key)
+    seeds, dirs = seeds[:sample], dirs[:sample]
+    for _ in range(max(args.warmup, 0) and 1):
+        cpu_numpy_port(ori, occ, seeds[: cores * 8], dirs[: cores * 8], params, cores)
+    rates, tot_t, tot_s = [], 0.0, 0
+    for _ in range(args.steps):
+        s, t = cpu_numpy_port(ori, occ, seeds, dirs, params, cores)
+        rates.append(s / t)
+        tot_t += t
+        tot_s += s
+    v = tot_s / tot_t
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "steps/s", "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": f"{cfg.name}: {cfg.note}", "sample_seeds": int(len(seeds)),
+                   "field": f"{cfg.n}^3 {cfg.kind}"},
+        "cpu_baseline": {"value": v, "unit": "steps/s", "cores": cores, "kind": "port",
+                         "sample": f"first {len(seeds)} seeds of {cfg.name} per step, numpy "
+                                   f"restatement of trace_batch in a {cores}-process fork pool "
+                                   f"(phg.py:184-207); host {model}"},
+        "e2e": {"value": v, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2604_05794_b200 import phg, synth
+    from paper_2604_05794_b200.volume import DeviceField
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = synth.CONFIGS[args.config]
+    per_rank = args.seeds or cfg.seeds
+    params = phg.PhgParams(field_seeds=0, batch_size=per_rank * ws)
+
+    # field generated directly in HBM, packed once (replicated per rank)
+    ori, occ = synth.make_field(cfg.kind, cfg.n, dev)
+    field = DeviceField(np.zeros(3), synth.VOXEL_MM, occ, ori,
+                        torch.cuda.current_stream(dev).cuda_stream)
+    ori_host = occ_host = None
+    if rank == 0 and not args.no_cpu:
+        ori_host, occ_host = ori.cpu().numpy(), occ.cpu().numpy()
+    del ori, occ
+    torch.cuda.empty_cache()
+
+    all_seeds, all_dirs = synth.disk_seeds(cfg.n, per_rank * ws, cfg.key)
+    s_host = np.ascontiguousarray(all_seeds[rank * per_rank:(rank + 1) * per_rank])
+    d_host = np.ascontiguousarray(all_dirs[rank * per_rank:(rank + 1) * per_rank])
+    s_dev = torch.from_numpy(s_host).to(dev)
+    d_dev = torch.from_numpy(d_host).to(dev)
+    stream = torch.cuda.current_stream(dev)
+    tracer = phg.Tracer()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+
+    def step():
+        off, verts, ent = phg.trace_device(field, s_dev, d_dev, params, tracer=tracer,
+                                           stream=stream)
+        if ws > 1:
+            mine = torch.tensor([per_rank, int(verts.shape[0])], dtype=torch.int64, device=dev)
+            allc = [torch.empty_like(mine) for _ in range(ws)]
+            dist.all_gather(allc, mine)
+        return off, verts
+
+    for _ in range(args.warmup):
+        flush.zero_()
+        off, verts = step()
+    torch.cuda.synchronize()
+    steps_per_trace = int(verts.shape[0]) - per_rank  # sum(len - 1) over returned strands
+    accepted = tracer.last_steps()
+    del off, verts
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    kern_ms = []
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        flush.zero_()
+        off, verts = step()
+        kern_ms.append(tracer.last_kernel_ms()[0])
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    ms = e0.elapsed_time(e1) / args.steps
+    clk = clocks.stop()
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if ws > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    total_steps = steps_per_trace * ws
+    value = total_steps / (ms_max / 1e3)
+    del off, verts
+
+    # e2e: host (pinned) buffers through the C ABI, copies inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        e2e = e2e_leg(args, tracer, field, params, s_host, d_host, per_rank, ws, dev, steps_per_trace)
+
+    kernel_ms = float(np.mean(kern_ms))
+    peak, peak_kind = measured_peak()
+    achieved = accepted * BYTES_PER_STEP / (kernel_ms / 1e3) / 1e9
+    traffic, traffic_steps = ncu_traffic()
+    if traffic is not None and traffic_steps:
+        traffic = traffic * accepted / traffic_steps
+
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        cores, model = cpu_host_info()
+        sample = args.cpu_sample or max(1024, cores * 256)
+        s_cpu, t_cpu = cpu_numpy_port(ori_host, occ_host, s_host[:sample], d_host[:sample],
+                                      params, cores)
+        c_s, c_t = cpu_c_port(ori_host, occ_host, s_host[: sample * 4], d_host[: sample * 4],
+                              params, cores)
+        cpu = {"value": s_cpu / t_cpu, "unit": "steps/s", "cores": cores, "kind": "port",
+               "sample": f"first {min(sample, per_rank)} seeds of {cfg.name} (numpy restatement "
+                         f"of trace_batch, {cores}-process fork pool like phg.py:184-207); "
+                         f"host {model}",
+               "c_port_value": c_s / c_t,
+               "c_port_sample": f"first {min(sample * 4, per_rank)} seeds, C oracle, "
+                                f"{cores} OpenMP threads"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": f"{cfg.name}: {cfg.note}", "field": f"{cfg.n}^3 {cfg.kind}",
+                       "seeds_per_gpu": per_rank, "global_seeds": per_rank * ws,
+                       "max_vertices": params.max_vertices, "step_mm": params.step_mm,
+                       "batch_size": per_rank * ws, "parallelism": f"seed-partition x{ws}",
+                       "l2": "256 MiB flush write between timed steps; field 2 GiB > L2"},
+            "steps_per_trace": steps_per_trace, "accepted_steps_per_trace": accepted,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": "trace_kernel", "kernel_ms": kernel_ms,
+                         "bytes_per_step": BYTES_PER_STEP, "peak_source": peak_kind},
+            "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
+            "gpu_launches": args.steps * phg.LAUNCHES_PER_TRACE,
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+def e2e_leg(args, tracer, field, params, s_host, d_host, per_rank, ws, dev, steps_per_trace):
+    """Seeds from pinned host memory in, full CSR (offsets, entered, verts) out to pinned host."""
+    import torch
+    import torch.distributed as dist
+
+    pin_s = torch.from_numpy(s_host).pin_memory()
+    pin_d = torch.from_numpy(d_host).pin_memory()
+    n = per_rank
+    out_off = torch.empty(n + 1, dtype=torch.int64).pin_memory()
+    out_ent = torch.empty(n, dtype=torch.uint8).pin_memory()
+    stream = torch.cuda.current_stream(dev)
+    total = tracer.trace(field, params, pin_s.data_ptr(), pin_d.data_ptr(), n,
+                         out_off.data_ptr(), out_ent.data_ptr(), None, stream.cuda_stream)
+    out_v = torch.empty((total, 3), dtype=torch.float64).pin_memory()
+
+    def one():
+        t = tracer.trace(field, params, pin_s.data_ptr(), pin_d.data_ptr(), n, out_off.data_ptr(),
+                         out_ent.data_ptr(), None, stream.cuda_stream)
+        tracer.gather(out_v.data_ptr(), t, stream.cuda_stream)
+        return t
+
+    for _ in range(max(1, args.warmup - 1)):
+        one()
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        total = one()
+    torch.cuda.synchronize()
+    dt = (time.perf_counter() - t0) / args.steps
+    tt = torch.tensor([dt], dtype=torch.float64, device=dev)
+    if ws > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    dt = float(tt.item())
+    return {"value": steps_per_trace * ws / dt, "unit": "steps/s",
+            "h2d_bytes_per_step": int(2 * n * 24), "d2h_bytes_per_step": int((n + 1) * 8 + n +
+                                                                             total * 24),
+            "ms_per_step": dt * 1e3,
+            "path": "phg_trace + phg_gather (C ABI) with pinned host seeds and host CSR output"}
+
+
+if __name__ == "__main__":
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)

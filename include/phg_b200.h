@@ -1,0 +1,115 @@
+/*
+ * phg_b200.h -- C ABI of the B200-native PHG (Parallel Hair Growing) tracer.
+ *
+ * Drop-in for the reference's grow-step boundary
+ *   strandkit.phg.trace_batch(vol, seed_pos, seed_dir, params,
+ *                             at_cap=None, live_counts=None, near_occ=None)
+ *   (/root/reference/pkg/src/strandkit/phg.py:67-163)
+ * and its sampler
+ *   strandkit.volume.sample_orientation_batch(vol, pts, prev_dirs)
+ *   (/root/reference/pkg/src/strandkit/volume.py:183-224).
+ * The reference has no FFI of its own (pure Python); the binding a maintainer
+ * adds is a ctypes stub that replaces the module attribute
+ * strandkit.phg.trace_batch, which every caller resolves at call time
+ * (phg.py:233,240,283,288).
+ *
+ * Conventions: plain pointers and sizes only.  Every array pointer may be a
+ * HOST pointer (pageable or pinned) or a DEVICE pointer of the field's GPU;
+ * the library detects which and stages host data itself.  `stream` is a
+ * cudaStream_t passed as void* (NULL = legacy default stream).  Functions never
+ * throw; they return a phg_status and phg_last_error() describes the failure
+ * (thread-local).  Arithmetic is IEEE binary64 in the reference's own
+ * evaluation order, so results are bit-identical to the reference.
+ */
+#ifndef PHG_B200_H
+#define PHG_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PHG_ABI_VERSION 1
+
+typedef enum {
+    PHG_OK = 0,
+    PHG_ERR_INVALID = 1,  /* bad argument / shape     -> strandkit DataError / ConfigError */
+    PHG_ERR_CUDA = 2,     /* CUDA runtime failure     -> strandkit PipelineError */
+    PHG_ERR_OOM = 3,      /* device allocation failed -> strandkit PipelineError */
+    PHG_ERR_CAPACITY = 4, /* caller output buffer too small (required size reported) */
+    PHG_ERR_STATE = 5     /* call order violated (e.g. gather before trace) */
+} phg_status;
+
+/* Packed, device-resident orientation/occupancy field (OOVolume, volume.py:21-56). */
+typedef struct phg_field phg_field;
+/* Per-caller context: scratch memory and the result of the last trace. */
+typedef struct phg_ctx phg_ctx;
+
+/* Trace parameters: the trace-relevant subset of PhgParams (phg.py:24-43). */
+typedef struct {
+    double step_mm;       /* PhgParams.step_mm */
+    double min_support;   /* PhgParams.min_support */
+    double steer;         /* PhgParams.steer (used only when a near-occupancy map is set) */
+    int32_t max_vertices; /* PhgParams.max_vertices (>= 1) */
+    int32_t probe_steps;  /* PhgParams.probe_steps */
+    int32_t coast_steps;  /* PhgParams.coast_steps */
+    uint32_t flags;       /* PHG_FLAG_* */
+} phg_params_v1;
+
+#define PHG_FLAG_STRICT 0x1u   /* PhgParams.strict: lockstep per-step commits to live_counts */
+#define PHG_FLAG_NO_ORDER 0x2u /* disable the locality (Morton) seed ordering; output order is
+                                  seed order either way */
+
+/* ---- field (replaces the OOVolume arrays read by volume.py:205-212) ---------- */
+
+/* ori: (nx,ny,nz,3) float32 C-order; occ: (nx,ny,nz) bool/uint8.  Copied and packed
+ * to float4 (ori.xyz, occ) on the current device. nx*ny*nz must be < 2^32. */
+phg_status phg_field_create(phg_field** out, const float* ori, const uint8_t* occ, int64_t nx,
+                            int64_t ny, int64_t nz, const double origin[3], double voxel_size,
+                            void* stream);
+/* at_cap: (nx,ny,nz) bool plane (phg.py:236) or NULL to clear.  Stored as a 1-bit plane. */
+phg_status phg_field_set_cap(phg_field* f, const uint8_t* at_cap, void* stream);
+/* near_occ: (nx,ny,nz,3) int64 nearest-occupied map (phg.py:57-64) or NULL to clear. */
+phg_status phg_field_set_near(phg_field* f, const int64_t* near_occ, void* stream);
+phg_status phg_field_destroy(phg_field* f);
+/* dims / device of a field (for callers' validation) */
+phg_status phg_field_info(const phg_field* f, int64_t dims[3], int* device);
+
+/* ---- context ---------------------------------------------------------------- */
+phg_status phg_ctx_create(phg_ctx** out);
+phg_status phg_ctx_destroy(phg_ctx* c);
+
+/* ---- trace (replaces trace_batch, phg.py:67-163) ----------------------------
+ * Phase 1: trace n seeds.  seed_pos/seed_dir: (n,3) float64.  live_counts:
+ * (nx,ny,nz) uint16, read and updated in place in strict mode (phg.py:150-154),
+ * ignored otherwise (may be NULL; strict mode then starts from zeros).
+ * Writes offsets (n+1) int64 (CSR row starts of the kept vertices, phg.py:159-162)
+ * and entered (n) uint8, and returns the total kept vertex count in *n_verts_out.
+ * Blocks until *n_verts_out is known (offsets/entered copies are complete on return). */
+phg_status phg_trace(phg_ctx* c, const phg_field* f, const phg_params_v1* p,
+                     const double* seed_pos, const double* seed_dir, int64_t n,
+                     uint16_t* live_counts, int64_t* offsets, uint8_t* entered,
+                     int64_t* n_verts_out, void* stream);
+/* Phase 2: write the kept vertices of the last phg_trace on this context as a
+ * (n_verts,3) float64 CSR payload.  verts_cap is in vertices. Blocks when verts is host memory. */
+phg_status phg_gather(phg_ctx* c, double* verts, int64_t verts_cap, void* stream);
+
+/* Per-strand raw counters of the last trace (diagnostics / step accounting):
+ * steps (n) int64 = integration steps each strand accepted (vertices appended). */
+phg_status phg_last_steps(phg_ctx* c, int64_t* total_steps);
+
+/* ---- sampler (replaces sample_orientation_batch, volume.py:183-224) --------- */
+phg_status phg_sample(const phg_field* f, const double* pts, const double* prev, int64_t n,
+                      double* dirs, uint8_t* has, double* support, void* stream);
+
+/* ---- diagnostics -------------------------------------------------------------- */
+const char* phg_last_error(void);
+int phg_abi_version(void);
+/* device time (ms) of the last trace kernel launch on this context (CUDA events on `stream`) */
+phg_status phg_last_kernel_ms(phg_ctx* c, float* trace_ms, float* total_ms);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PHG_B200_H */

@@ -1,0 +1,118 @@
+"""ctypes binding of libphg_b200.so (the C ABI declared in include/phg_b200.h).
+
+The shared library is built in-tree by ``__graft_entry__.build()`` /
+``python -m paper_2604_05794_b200.build``.  There is NO fallback: if the
+library is missing or fails to load, every entry point raises
+``PipelineError`` -- the product path never silently runs on the CPU.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+from .errors import ConfigError, DataError, PipelineError
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libphg_b200.so")
+
+PHG_OK, PHG_ERR_INVALID, PHG_ERR_CUDA, PHG_ERR_OOM, PHG_ERR_CAPACITY, PHG_ERR_STATE = range(6)
+PHG_FLAG_STRICT = 0x1
+PHG_FLAG_NO_ORDER = 0x2
+
+# every symbol include/phg_b200.h declares (checked by tests/test_native_abi.py)
+EXPORTS = (
+    "phg_field_create", "phg_field_set_cap", "phg_field_set_near", "phg_field_destroy",
+    "phg_field_info", "phg_ctx_create", "phg_ctx_destroy", "phg_trace", "phg_gather",
+    "phg_last_steps", "phg_sample", "phg_last_error", "phg_abi_version", "phg_last_kernel_ms",
+)
+
+
+class Params(ctypes.Structure):
+    """phg_params_v1"""
+
+    _fields_ = [
+        ("step_mm", ctypes.c_double),
+        ("min_support", ctypes.c_double),
+        ("steer", ctypes.c_double),
+        ("max_vertices", ctypes.c_int32),
+        ("probe_steps", ctypes.c_int32),
+        ("coast_steps", ctypes.c_int32),
+        ("flags", ctypes.c_uint32),
+    ]
+
+
+_lib = None
+_load_error = None
+
+VP = ctypes.c_void_p
+I64 = ctypes.c_int64
+
+
+def _declare(lib):
+    S = ctypes.c_int
+    sig = {
+        "phg_field_create": (S, [ctypes.POINTER(VP), VP, VP, I64, I64, I64,
+                                 ctypes.POINTER(ctypes.c_double), ctypes.c_double, VP]),
+        "phg_field_set_cap": (S, [VP, VP, VP]),
+        "phg_field_set_near": (S, [VP, VP, VP]),
+        "phg_field_destroy": (S, [VP]),
+        "phg_field_info": (S, [VP, ctypes.POINTER(I64), ctypes.POINTER(ctypes.c_int)]),
+        "phg_ctx_create": (S, [ctypes.POINTER(VP)]),
+        "phg_ctx_destroy": (S, [VP]),
+        "phg_trace": (S, [VP, VP, ctypes.POINTER(Params), VP, VP, I64, VP, VP, VP,
+                          ctypes.POINTER(I64), VP]),
+        "phg_gather": (S, [VP, VP, I64, VP]),
+        "phg_last_steps": (S, [VP, ctypes.POINTER(I64)]),
+        "phg_sample": (S, [VP, VP, VP, I64, VP, VP, VP, VP]),
+        "phg_last_error": (ctypes.c_char_p, []),
+        "phg_abi_version": (ctypes.c_int, []),
+        "phg_last_kernel_ms": (S, [VP, ctypes.POINTER(ctypes.c_float),
+                                   ctypes.POINTER(ctypes.c_float)]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+
+
+def load():
+    """Load (once) and return the native library; raise PipelineError if unavailable."""
+    global _lib, _load_error
+    if _lib is not None:
+        return _lib
+    if _load_error is not None:
+        raise PipelineError(_load_error)
+    if not os.path.exists(LIB_PATH):
+        _load_error = (f"native PHG library not built: {LIB_PATH} is missing "
+                       "(run `python -m paper_2604_05794_b200.build`)")
+        raise PipelineError(_load_error)
+    try:
+        lib = ctypes.CDLL(LIB_PATH)
+        _declare(lib)
+    except OSError as e:
+        _load_error = f"cannot load {LIB_PATH}: {e}"
+        raise PipelineError(_load_error) from e
+    _lib = lib
+    return lib
+
+
+def check(status: int, what: str):
+    if status == PHG_OK:
+        return
+    msg = f"{what}: {_lib.phg_last_error().decode(errors='replace')}"
+    if status == PHG_ERR_INVALID:
+        raise DataError(msg)
+    if status in (PHG_ERR_CAPACITY, PHG_ERR_STATE):
+        raise PipelineError(msg)
+    raise PipelineError(msg)
+
+
+def params_struct(p, strict=None, order=True) -> Params:
+    mv = int(p.max_vertices)
+    if mv < 1:
+        raise ConfigError(f"max_vertices must be >= 1 (got {mv})")
+    st = bool(p.strict) if strict is None else strict
+    flags = (PHG_FLAG_STRICT if st else 0) | (0 if order else PHG_FLAG_NO_ORDER)
+    return Params(float(p.step_mm), float(p.min_support), float(getattr(p, "steer", 0.0)), mv,
+                  int(p.probe_steps), int(p.coast_steps), flags)

@@ -1,0 +1,238 @@
+"""Drop-in PHG grow step on B200: ``trace_batch`` with the reference's signature.
+
+Reference boundary (strandkit/phg.py:67-163)::
+
+    trace_batch(vol, seed_pos, seed_dir, params, at_cap=None, live_counts=None,
+                near_occ=None) -> [(vertices (k,3) float64, entered bool), ...]
+
+Every caller in the reference (init_guide_strands phg.py:233,240;
+_trace_field_seeds.run_dir phg.py:283,288; the fork worker phg.py:180)
+resolves ``trace_batch`` as a module global at call time, so ``install()``
+reroutes the whole grow stage through the GPU by attribute replacement.
+
+The arithmetic runs in libphg_b200.so (csrc/phg_trace.cu) -- IEEE binary64
+in the reference's evaluation order, bit-identical output.  All modes run on
+the GPU: relaxed (frozen ``at_cap`` plane), strict (lockstep per-step commits
+to ``live_counts``) and steering (``near_occ`` with ``steer > 0``).  There is
+no CPU fallback: without the native library every call raises PipelineError.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native
+from .errors import ConfigError, DataError
+from .volume import field_for
+
+
+@dataclass
+class PhgParams:
+    """Mirror of strandkit.phg.PhgParams (phg.py:24-51): same fields, defaults, checks."""
+
+    step_mm: float = 1.0
+    max_vertices: int = 400
+    batch_size: int = 16384
+    occupancy_cap: int = 16
+    link_dist_mm: float = 2.0
+    link_angle_deg: float = 30.0
+    n_root: int = 30000
+    attach_radius_mm: float = 10.0
+    probe_steps: int = 24
+    min_support: float = 0.05
+    coast_steps: int = 25
+    steer: float = 0.0
+    field_seeds: int = 30000
+    smooth: bool = True
+    smooth_strength: float = 0.25
+    smooth_iters: int = 2
+    strict: bool = False
+    tangent_window: int = 3
+
+    def __post_init__(self):
+        if self.link_dist_mm <= 0:
+            raise ConfigError("link_dist_mm must be positive")
+        if not (0 < self.link_angle_deg < 90):
+            raise ConfigError("link_angle_deg must be in (0, 90)")
+        if self.step_mm <= 0 or self.batch_size < 1 or self.occupancy_cap < 1:
+            raise ConfigError("invalid tracing parameters")
+
+
+class Tracer:
+    """Owns a native context (scratch + last result). One per thread/stream."""
+
+    def __init__(self):
+        self._lib = _native.load()
+        h = ctypes.c_void_p()
+        _native.check(self._lib.phg_ctx_create(ctypes.byref(h)), "phg_ctx_create")
+        self.handle = h
+
+    def close(self):
+        if self.handle:
+            self._lib.phg_ctx_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
+
+    def trace(self, field, params, seed_pos, seed_dir, n, offsets_ptr, entered_ptr,
+              live_counts_ptr=None, stream=0, order=True):
+        """Phase 1 (phg_trace). Pointers may be host or device. Returns total kept vertices."""
+        p = _native.params_struct(params, order=order)
+        total = ctypes.c_int64()
+        _native.check(self._lib.phg_trace(self.handle, field.handle, ctypes.byref(p), seed_pos,
+                                          seed_dir, n, live_counts_ptr, offsets_ptr, entered_ptr,
+                                          ctypes.byref(total), stream), "phg_trace")
+        return int(total.value)
+
+    def gather(self, verts_ptr, cap, stream=0):
+        _native.check(self._lib.phg_gather(self.handle, verts_ptr, cap, stream), "phg_gather")
+
+    def last_steps(self):
+        v = ctypes.c_int64()
+        _native.check(self._lib.phg_last_steps(self.handle, ctypes.byref(v)), "phg_last_steps")
+        return int(v.value)
+
+    def last_kernel_ms(self):
+        a, b = ctypes.c_float(), ctypes.c_float()
+        _native.check(self._lib.phg_last_kernel_ms(self.handle, ctypes.byref(a), ctypes.byref(b)),
+                      "phg_last_kernel_ms")
+        return float(a.value), float(b.value)
+
+
+# Kernel launches of one relaxed-mode phg_trace + phg_gather from libphg_b200.so:
+# morton keys, CUB radix sort (onesweep: histogram + 4 passes), trace, CUB scan (2), gather.
+LAUNCHES_PER_TRACE = 10
+
+_TRACER = None
+
+
+def _tracer():
+    global _TRACER
+    if _TRACER is None:
+        _TRACER = Tracer()
+    return _TRACER
+
+
+def _seeds(a, name):
+    a = np.ascontiguousarray(np.asarray(a, dtype=np.float64).reshape(-1, 3))
+    return a
+
+
+def trace_batch_csr(vol, seed_pos, seed_dir, params, at_cap=None, live_counts=None,
+                    near_occ=None):
+    """trace_batch with CSR output: (offsets (n+1,) i64, verts (M,3) f64, entered (n,) bool).
+
+    Host numpy in, host numpy out; H2D/D2H staging happens inside the C ABI.
+    """
+    pos = _seeds(seed_pos, "seed_pos")
+    dirs = _seeds(seed_dir, "seed_dir")
+    n = len(pos)
+    if len(dirs) != n:
+        raise DataError(f"seed_pos ({n}) and seed_dir ({len(dirs)}) lengths differ")
+    if int(params.max_vertices) < 1:
+        raise ConfigError(f"max_vertices must be >= 1 (got {params.max_vertices})")
+    field = field_for(vol)
+    strict = bool(params.strict)
+    counts_ptr = None
+    if strict:
+        if live_counts is not None:
+            if not (isinstance(live_counts, np.ndarray) and live_counts.dtype == np.uint16
+                    and live_counts.flags.c_contiguous and live_counts.shape == field.dims):
+                raise DataError("live_counts must be a C-contiguous uint16 array of the field dims")
+            counts_ptr = live_counts.ctypes.data
+        field.set_cap(None)
+    else:
+        cap = at_cap
+        if cap is not None and isinstance(cap, np.ndarray) and not cap.any():
+            cap = None  # an all-False plane never stops a strand (phg.py:139-142)
+        field.set_cap(cap)
+    steer = near_occ is not None and float(params.steer) > 0
+    field.set_near(near_occ if steer else None)
+    offsets = np.zeros(n + 1, np.int64)
+    entered = np.zeros(n, np.uint8)
+    tr = _tracer()
+    total = tr.trace(field, params, pos.ctypes.data if n else None,
+                     dirs.ctypes.data if n else None, n, offsets.ctypes.data,
+                     entered.ctypes.data if n else None, counts_ptr)
+    verts = np.empty((total, 3))
+    if total:
+        tr.gather(verts.ctypes.data, total)
+    return offsets, verts, entered.astype(bool)
+
+
+def trace_batch(vol, seed_pos, seed_dir, params, at_cap=None, live_counts=None, near_occ=None):
+    """GPU drop-in for strandkit.phg.trace_batch (phg.py:67-163).
+
+    Returns a list of ``(vertices (k,3) float64, entered bool)`` in seed order;
+    each ``vertices`` is a C-contiguous row block of one CSR payload.
+    """
+    offsets, verts, entered = trace_batch_csr(vol, seed_pos, seed_dir, params, at_cap=at_cap,
+                                              live_counts=live_counts, near_occ=near_occ)
+    parts = np.split(verts, offsets[1:-1]) if len(entered) else []
+    return list(zip(parts, entered.tolist()))
+
+
+def trace_device(field, seed_pos, seed_dir, params, tracer=None, stream=None, order=True):
+    """Zero-copy device API: torch CUDA tensors in, torch CUDA tensors out.
+
+    ``field`` is a DeviceField (cap / near planes already set); seeds are (n,3)
+    float64 CUDA tensors.  Returns (offsets (n+1,) i64, verts (M,3) f64,
+    entered (n,) u8) on the same device, all produced on ``stream``.
+    """
+    import torch
+
+    tr = tracer or _tracer()
+    n = int(seed_pos.shape[0])
+    dev = seed_pos.device
+    st = stream if stream is not None else torch.cuda.current_stream(dev)
+    offsets = torch.empty(n + 1, dtype=torch.int64, device=dev)
+    entered = torch.empty(max(n, 1), dtype=torch.uint8, device=dev)[:n]
+    total = tr.trace(field, params, seed_pos.data_ptr() if n else None,
+                     seed_dir.data_ptr() if n else None, n, offsets.data_ptr(),
+                     entered.data_ptr() if n else None, None, st.cuda_stream, order=order)
+    verts = torch.empty((total, 3), dtype=torch.float64, device=dev)
+    if total:
+        tr.gather(verts.data_ptr(), total, st.cuda_stream)
+    return offsets, verts, entered
+
+
+# ----------------------------------------------------------------------------------
+# installation into the reference package
+# ----------------------------------------------------------------------------------
+_SAVED = {}
+
+
+def install(module=None):
+    """Reroute the reference grow stage through the GPU.
+
+    Replaces ``strandkit.phg.trace_batch`` (resolved as a module global by
+    every caller) and disables the fork pool (``_make_pool`` -> None,
+    phg.py:184-196) because CUDA state must not be inherited by forked workers;
+    the batch loop then calls trace_batch in-process (phg.py:239-241).
+    """
+    if module is None:
+        import strandkit.phg as module  # type: ignore
+    if module in _SAVED:
+        return module
+    _SAVED[module] = (module.trace_batch, getattr(module, "_make_pool", None))
+    module.trace_batch = trace_batch
+    if hasattr(module, "_make_pool"):
+        module._make_pool = lambda *a, **k: None
+    return module
+
+
+def uninstall(module=None):
+    if module is None:
+        import strandkit.phg as module  # type: ignore
+    saved = _SAVED.pop(module, None)
+    if saved:
+        module.trace_batch = saved[0]
+        if saved[1] is not None:
+            module._make_pool = saved[1]

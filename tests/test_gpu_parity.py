@@ -1,0 +1,255 @@
+"""Parity of the CUDA path (through the C ABI) with the reference and the oracle.
+
+Bar: bit-exact.  The kernel computes in IEEE binary64 in the reference's
+evaluation order (csrc/phg_trace.cu), so every vertex of every strand must be
+identical to the reference's (golden fixtures) and to the oracle's at larger
+sizes; the north_star tolerance (counts exact >= 99.9 %, positions <= 1e-3
+voxel) is reported alongside as the weaker, stated bar.
+"""
+
+import os
+from types import SimpleNamespace
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, csr_equal, load_case, trace_cases
+
+pytestmark = pytest.mark.gpu
+
+CASES = trace_cases()
+
+
+@pytest.fixture(scope="module")
+def gpu():
+    import torch
+
+    from paper_2604_05794_b200 import _native, build
+
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    build.build()
+    _native.load()
+    from paper_2604_05794_b200 import phg, volume
+
+    return SimpleNamespace(phg=phg, volume=volume, torch=torch)
+
+
+def run_gpu(gpu, c, live_counts=None):
+    return gpu.phg.trace_batch_csr(c.vol, c.seeds, c.dirs, c.params,
+                                   at_cap=getattr(c, "at_cap", None), live_counts=live_counts,
+                                   near_occ=getattr(c, "near_occ", None))
+
+
+def tolerance_report(off_a, v_a, off_b, v_b, vs):
+    la, lb = np.diff(off_a), np.diff(off_b)
+    same = la == lb
+    err = 0.0
+    for i in np.flatnonzero(same)[:: max(1, int(same.sum()) // 2000)]:
+        a = v_a[off_a[i]:off_a[i + 1]]
+        b = v_b[off_b[i]:off_b[i + 1]]
+        if len(a):
+            err = max(err, float(np.abs(a - b).max()) / vs)
+    return float(same.mean()) if len(same) else 1.0, err
+
+
+@pytest.mark.parametrize("path", CASES, ids=lambda p: os.path.basename(p)[6:-4])
+def test_cuda_matches_reference_golden(gpu, path):
+    c = load_case(path)
+    counts = c.counts_in.copy() if hasattr(c, "counts_in") else None
+    off, v, ent = run_gpu(gpu, c, live_counts=counts)
+    assert np.array_equal(ent, c.entered)
+    assert csr_equal(off, v, c.offsets, c.verts), tolerance_report(off, v, c.offsets, c.verts,
+                                                                   float(c.voxel_size))
+    if counts is not None:
+        assert np.array_equal(counts, c.counts_out)
+
+
+def test_cuda_list_output_is_reference_shaped(gpu):
+    c = load_case(os.path.join(GOLDEN, "trace_sparse48.npz"))
+    out = gpu.phg.trace_batch(c.vol, c.seeds, c.dirs, c.params)
+    assert len(out) == len(c.entered)
+    for i, (v, e) in enumerate(out):
+        assert v.dtype == np.float64 and v.ndim == 2 and v.shape[1] == 3
+        assert v.flags.c_contiguous
+        assert e is bool(c.entered[i])
+        assert np.array_equal(v, c.verts[c.offsets[i]:c.offsets[i + 1]])
+
+
+def test_cuda_sampler_matches_reference_golden(gpu):
+    c = load_case(os.path.join(GOLDEN, "sample_sparse24.npz"))
+    d, h, s = gpu.volume.sample_orientation_batch(c.vol, c.pts, c.prev)
+    assert np.array_equal(h, c.has)
+    assert np.array_equal(s, c.support)
+    assert np.array_equal(d, c.dirs)
+
+
+def test_sampler_sign_follows_query(gpu):
+    """test_volume.py:58-67 analog: flipping prev flips the sampled direction."""
+    c = load_case(os.path.join(GOLDEN, "sample_sparse24.npz"))
+    d1, h1, _ = gpu.volume.sample_orientation_batch(c.vol, c.pts, c.prev)
+    d2, h2, _ = gpu.volume.sample_orientation_batch(c.vol, c.pts, -c.prev)
+    assert np.array_equal(h1, h2)
+    assert np.allclose(d1[h1], -d2[h1], atol=1e-12)
+
+
+# ---- larger sizes: GPU vs the C oracle on the BASELINE configs ----------------------
+def _config_case(kind, n, count, key, params=None, seeds=None, interior=0):
+    from paper_2604_05794_b200 import synth
+
+    ori, occ = synth.make_field(kind, n, "cpu")
+    ori, occ = ori.numpy(), occ.numpy()
+    if seeds is None:
+        s, d = synth.disk_seeds(n, count, key)
+    else:
+        s, d = seeds
+    if interior:
+        s2, d2 = synth.interior_seeds(occ, ori, interior, key + 100)
+        s, d = np.concatenate([s, s2, s2]), np.concatenate([d, d2, -d2])
+    p = params or SimpleNamespace(step_mm=1.0, max_vertices=400, min_support=0.05,
+                                  probe_steps=24, coast_steps=25, steer=0.0, strict=False)
+    vol = SimpleNamespace(origin=np.zeros(3), voxel_size=synth.VOXEL_MM, dims=occ.shape, occ=occ,
+                          ori=ori)
+    return vol, s, d, p
+
+
+def _compare_with_oracle(gpu, oracle_c, vol, s, d, p, at_cap=None):
+    off, v, ent = gpu.phg.trace_batch_csr(vol, s, d, p, at_cap=at_cap)
+    slab, keep, ent_o = oracle_c.trace(vol.origin, vol.voxel_size, vol.occ, vol.ori, s, d, p,
+                                       at_cap=at_cap)
+    off_o, v_o = oracle_c.to_csr(slab, keep)
+    frac, err = tolerance_report(off, v, off_o, v_o, vol.voxel_size)
+    assert frac >= 0.999 and err <= 1e-3, (frac, err)  # north_star bar
+    assert np.array_equal(ent, ent_o)
+    assert csr_equal(off, v, off_o, v_o)  # our bar: bit-exact
+    return off
+
+
+def test_c1_straight_full_10k_bit_exact(gpu, oracle_c):
+    vol, s, d, p = _config_case("straight", 64, 10_000, 11)
+    off = _compare_with_oracle(gpu, oracle_c, vol, s, d, p)
+    assert (np.diff(off) - 1).sum() > 1_000_000
+
+
+def test_c2_wavy_256_subset_bit_exact(gpu, oracle_c):
+    vol, s, d, p = _config_case("wavy", 256, 2_000, 12)
+    _compare_with_oracle(gpu, oracle_c, vol, s, d, p)
+
+
+def test_c3_curly_512_subset_bit_exact(gpu, oracle_c):
+    vol, s, d, p = _config_case("curly", 512, 1_000, 13)
+    off = _compare_with_oracle(gpu, oracle_c, vol, s, d, p)
+    assert np.all(np.diff(off) >= 300)
+
+
+def test_c5_sparse_divergent_lengths_bit_exact(gpu, oracle_c):
+    vol, s, d, p = _config_case("sparse", 96, 3_000, 15, interior=3_000)
+    off = _compare_with_oracle(gpu, oracle_c, vol, s, d, p)
+    lens = np.diff(off)
+    assert lens.max() > 4 * np.median(lens)  # the stress case really is divergent
+
+
+def test_nonempty_cap_plane_bit_exact(gpu, oracle_c):
+    vol, s, d, p = _config_case("curly", 64, 5_000, 16)
+    rng = np.random.Generator(np.random.Philox(key=3))
+    cap = rng.random(vol.occ.shape) < 0.02
+    _compare_with_oracle(gpu, oracle_c, vol, s, d, p, at_cap=cap)
+
+
+def test_seed_order_does_not_change_results(gpu):
+    """Locality ordering is scheduling only: seed i's strand is the same at any position."""
+    vol, s, d, p = _config_case("sparse", 64, 6_000, 17, interior=1_000)
+    off, v, e = gpu.phg.trace_batch_csr(vol, s, d, p)
+    perm = np.random.Generator(np.random.Philox(key=4)).permutation(len(s))
+    off2, v2, e2 = gpu.phg.trace_batch_csr(vol, s[perm], d[perm], p)
+    for k, i in enumerate(perm[:500]):
+        assert np.array_equal(v[off[i]:off[i + 1]], v2[off2[k]:off2[k + 1]])
+        assert e[i] == e2[k]
+
+
+# ---- the reference's own trace tests, run against the GPU drop-in ---------------------
+def _column(height=40):
+    from paper_2604_05794_b200.volume import OOVolume
+
+    vol = OOVolume.empty(origin=(-10.0, -10.0, 0.0), voxel_size=2.0, dims=(10, 10, height))
+    vol.occ[:] = True
+    vol.ori[:] = np.asarray((0.0, 0.0, 1.0), dtype=np.float32)
+    return vol
+
+
+def test_reference_unit_tests_on_gpu(gpu):
+    """test_phg.py:33-127 restated against the GPU trace_batch."""
+    P = gpu.phg.PhgParams
+    tb = gpu.phg.trace_batch
+    up, s0 = [[0.0, 0.0, 1.0]], [[0.5, 0.5, 1.0]]
+    (v, e), = tb(_column(), s0, up, P(max_vertices=30, probe_steps=0, coast_steps=0))
+    assert e and len(v) >= 29 and np.allclose(v[:, :2], [0.5, 0.5], atol=1e-9)
+    assert np.allclose(np.diff(v[:, 2]), 1.0)
+    (v, e), = tb(_column(5), s0, up, P(max_vertices=60, probe_steps=0, coast_steps=0))
+    assert e and len(v) < 20
+    vol = _column()
+    vol.occ[:, :, :6] = False
+    (_, e1), = tb(vol, s0, up, P(max_vertices=40, probe_steps=2, coast_steps=0))
+    (v, e2), = tb(vol, s0, up, P(max_vertices=40, probe_steps=15, coast_steps=0))
+    assert not e1 and e2 and len(v) > 20
+    vol = _column()
+    vol.occ[:, :, 10:13] = False
+    (vn, _), = tb(vol, s0, up, P(max_vertices=90, probe_steps=0, coast_steps=0))
+    (vy, _), = tb(vol, s0, up, P(max_vertices=90, probe_steps=0, coast_steps=12))
+    assert vy[-1, 2] > 40.0 and vn[-1, 2] < 25.0
+    (v, e), = tb(_column(10), s0, up, P(max_vertices=80, probe_steps=0, coast_steps=10))
+    assert e and v[-1, 2] < 22.5
+    counts = np.zeros((10, 10, 40), np.uint16)
+    out = tb(_column(), [[0.5, 0.5, 1.0], [0.5, 0.5, 0.2]], up + up,
+             P(max_vertices=30, probe_steps=0, coast_steps=0, strict=True), live_counts=counts)
+    assert len(out[0][0]) >= 29 and len(out[1][0]) < 5 and counts.sum() > 0
+    cap = np.zeros((10, 10, 40), bool)
+    out = tb(_column(), np.tile(s0, (4, 1)), np.tile(up, (4, 1)),
+             P(max_vertices=30, probe_steps=0, coast_steps=0, occupancy_cap=1), at_cap=cap)
+    assert all(len(v) >= 29 for v, _ in out)
+    cap[:, :, 8:] = True
+    (v, e), = tb(_column(), s0, up, P(max_vertices=30, probe_steps=0, coast_steps=0), at_cap=cap)
+    assert e and v[-1, 2] < 17.0
+
+
+def test_errors_map_to_reference_types(gpu):
+    from paper_2604_05794_b200.errors import ConfigError, DataError
+
+    vol = _column()
+    P = gpu.phg.PhgParams
+    with pytest.raises(DataError):
+        gpu.phg.trace_batch(vol, np.zeros((3, 3)), np.zeros((2, 3)), P())
+    with pytest.raises(ConfigError):
+        gpu.phg.trace_batch(vol, np.zeros((1, 3)), np.ones((1, 3)), P(max_vertices=0))
+    with pytest.raises(DataError):
+        gpu.phg.trace_batch(vol, np.zeros((1, 3)), np.ones((1, 3)), P(), at_cap=np.zeros((2, 2, 2)))
+    assert gpu.phg.trace_batch(vol, np.zeros((0, 3)), np.zeros((0, 3)), P()) == []
+
+
+def test_install_reroutes_module_global(gpu):
+    """install() replaces trace_batch on a reference-shaped module and disables the fork pool."""
+    import types
+
+    mod = types.ModuleType("fake_phg")
+    mod.trace_batch = lambda *a, **k: "cpu"
+    mod._make_pool = lambda *a, **k: "pool"
+    gpu.phg.install(mod)
+    try:
+        assert mod.trace_batch is gpu.phg.trace_batch
+        assert mod._make_pool(None, None, None, 8) is None
+    finally:
+        gpu.phg.uninstall(mod)
+    assert mod.trace_batch() == "cpu"
+
+
+def test_device_api_matches_host_api(gpu):
+    torch = gpu.torch
+    vol, s, d, p = _config_case("wavy", 64, 3_000, 18)
+    off, v, e = gpu.phg.trace_batch_csr(vol, s, d, p)
+    f = gpu.volume.field_for(vol)
+    f.set_cap(None)
+    f.set_near(None)
+    o2, v2, e2 = gpu.phg.trace_device(f, torch.from_numpy(s).cuda(), torch.from_numpy(d).cuda(), p)
+    torch.cuda.synchronize()
+    assert np.array_equal(o2.cpu().numpy(), off)
+    assert np.array_equal(v2.cpu().numpy(), v)
+    assert np.array_equal(e2.cpu().numpy().astype(bool), e)

@@ -1,0 +1,86 @@
+"""The C-ABI library builds, loads without a GPU and exports every symbol the header declares."""
+
+import ctypes
+import os
+import re
+
+import pytest
+
+from conftest import ROOT
+
+HEADER = os.path.join(ROOT, "include", "phg_b200.h")
+
+
+def header_functions():
+    text = open(HEADER).read()
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?\w+\*?\s+\*?(phg_\w+)\s*\(", text, re.M)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2604_05794_b200 import _native, build
+
+    build.build()
+    return _native.load()
+
+
+def test_header_declares_entry_points():
+    names = header_functions()
+    assert "phg_trace" in names and "phg_field_create" in names and len(names) >= 12
+
+
+def test_library_exports_every_header_symbol(lib):
+    from paper_2604_05794_b200 import _native
+
+    for name in header_functions():
+        assert hasattr(lib, name), name
+    assert set(header_functions()) == set(_native.EXPORTS)
+
+
+def test_abi_version(lib):
+    assert lib.phg_abi_version() == 1
+
+
+def test_null_arguments_fail_cleanly_without_gpu(lib):
+    from paper_2604_05794_b200 import _native
+
+    assert lib.phg_field_create(None, None, None, 1, 1, 1, None, 1.0, None) == \
+        _native.PHG_ERR_INVALID
+    assert b"null" in lib.phg_last_error()
+    total = ctypes.c_int64()
+    assert lib.phg_trace(None, None, None, None, None, 0, None, None, None,
+                         ctypes.byref(total), None) == _native.PHG_ERR_INVALID
+    assert lib.phg_gather(None, None, 0, None) == _native.PHG_ERR_INVALID
+
+
+def test_sm100a_cubin_embedded():
+    import subprocess
+
+    from paper_2604_05794_b200 import build
+
+    out = subprocess.run(["cuobjdump", "--list-elf", build.OUT], capture_output=True, text=True)
+    if out.returncode != 0:
+        pytest.skip("cuobjdump unavailable")
+    assert "sm_100a" in out.stdout
+
+
+def test_params_mirror_validation():
+    from paper_2604_05794_b200.errors import ConfigError
+    from paper_2604_05794_b200.phg import PhgParams
+
+    for bad in (dict(link_dist_mm=0.0), dict(link_angle_deg=95.0), dict(step_mm=-1.0),
+                dict(occupancy_cap=0), dict(batch_size=0)):
+        with pytest.raises(ConfigError):
+            PhgParams(**bad)
+    p = PhgParams()
+    assert (p.step_mm, p.max_vertices, p.batch_size, p.occupancy_cap, p.probe_steps,
+            p.min_support, p.coast_steps) == (1.0, 400, 16384, 16, 24, 0.05, 25)
+
+
+def test_product_package_never_imports_oracle():
+    pkg = os.path.join(ROOT, "paper_2604_05794_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith(".py"):
+                src = open(os.path.join(dirpath, f)).read()
+                assert "oracle" not in re.sub(r"#.*|\"\"\"[\s\S]*?\"\"\"", "", src), f
