@@ -150,6 +150,8 @@ def trace_batch_csr(vol, seed_pos, seed_dir, params, at_cap=None, live_counts=No
         field.set_cap(None)
     else:
         cap = at_cap
+        if cap is not None and tuple(np.shape(cap)) != field.dims:
+            raise DataError(f"at_cap shape {tuple(np.shape(cap))} != field dims {field.dims}")
         if cap is not None and isinstance(cap, np.ndarray) and not cap.any():
             cap = None  # an all-False plane never stops a strand (phg.py:139-142)
         field.set_cap(cap)
