@@ -44,6 +44,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=0, help="seeds in the CPU sample")
+    ap.add_argument("--sweep", action="store_true", help="time every trace-kernel variant")
     return ap.parse_args()
 
 
@@ -250,6 +251,10 @@ def run_ours(args):
             dist.all_gather(allc, mine)
         return off, verts
 
+    if args.sweep:
+        sweep_variants(args, step, tracer, flush)
+        return
+
     for _ in range(args.warmup):
         flush.zero_()
         off, verts = step()
@@ -334,6 +339,37 @@ def run_ours(args):
         print(json.dumps(line), flush=True)
     if ws > 1:
         dist.destroy_process_group()
+
+
+def sweep_variants(args, step, tracer, flush):
+    """Time every compiled trace-kernel variant on this workload; check bit-identity."""
+    import torch
+
+    from paper_2604_05794_b200 import _native
+
+    ref = None
+    for v in range(_native.load().phg_num_variants()):
+        os.environ["PHG_VARIANT"] = str(v)
+        for _ in range(2):
+            flush.zero_()
+            off, verts = step()
+        ms = []
+        for _ in range(max(args.steps, 1)):
+            flush.zero_()
+            off, verts = step()
+            ms.append(tracer.last_kernel_ms()[0])
+        torch.cuda.synchronize()
+        if ref is None:
+            ref = (off.clone(), verts.clone())
+            same = True
+        else:
+            same = bool(torch.equal(ref[0], off) and torch.equal(ref[1], verts))
+        acc = tracer.last_steps()
+        print(json.dumps({"variant": v, "name": tracer.last_variant(), "kernel_ms": min(ms),
+                          "kernel_ms_all": ms, "gsteps_per_s": acc / min(ms) / 1e6,
+                          "identical_to_variant0": same}), flush=True)
+        del off, verts
+    os.environ.pop("PHG_VARIANT", None)
 
 
 def e2e_leg(args, tracer, field, params, s_host, d_host, per_rank, ws, dev, steps_per_trace):

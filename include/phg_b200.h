@@ -108,6 +108,10 @@ const char* phg_last_error(void);
 int phg_abi_version(void);
 /* device time (ms) of the last trace kernel launch on this context (CUDA events on `stream`) */
 phg_status phg_last_kernel_ms(phg_ctx* c, float* trace_ms, float* total_ms);
+/* name of the trace-kernel variant the last trace used (env PHG_VARIANT=<index> selects one;
+ * all variants are bit-identical) and the number of compiled variants */
+const char* phg_last_variant(phg_ctx* c);
+int phg_num_variants(void);
 
 #ifdef __cplusplus
 }

@@ -99,6 +99,9 @@ class Tracer:
         _native.check(self._lib.phg_last_steps(self.handle, ctypes.byref(v)), "phg_last_steps")
         return int(v.value)
 
+    def last_variant(self):
+        return self._lib.phg_last_variant(self.handle).decode()
+
     def last_kernel_ms(self):
         a, b = ctypes.c_float(), ctypes.c_float()
         _native.check(self._lib.phg_last_kernel_ms(self.handle, ctypes.byref(a), ctypes.byref(b)),
@@ -107,8 +110,9 @@ class Tracer:
 
 
 # Kernel launches of one relaxed-mode phg_trace + phg_gather from libphg_b200.so:
-# morton keys, CUB radix sort (onesweep: histogram + 4 passes), trace, CUB scan (2), gather.
-LAUNCHES_PER_TRACE = 10
+# morton keys, CUB radix sort (histogram, exclusive-sum, 4 onesweep passes), trace,
+# CUB scan (init + scan), gather -- as listed by ncu (profiles/r01_v0_launches.csv).
+LAUNCHES_PER_TRACE = 11
 
 _TRACER = None
 
