@@ -1,0 +1,79 @@
+"""World-size-2 gloo test of the multi-GPU host logic (seed slices + count exchange +
+rank-order concatenation), with the C oracle standing in for the per-rank GPU trace.
+
+Contract (A9 analogue, test_acceptance.py:302-334): the concatenated rank outputs equal
+the single-process output byte for byte.
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+from conftest import GOLDEN, ROOT, load_case
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, case_path, out_path):
+    import sys
+
+    sys.path.insert(0, ROOT)
+    import torch.distributed as dist
+
+    from oracle import phg_oracle_c as oc
+    from paper_2604_05794_b200 import dist as pdist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        c = load_case(case_path)
+
+        def trace_fn(pos, dirs):
+            slab, keep, ent = oc.trace(c.origin, c.voxel_size, c.occ, c.ori, pos, dirs, c.params)
+            off, v = oc.to_csr(slab, keep)
+            return off, v, ent
+
+        off_g, verts, ent, info = pdist.trace_sharded(trace_fn, c.seeds, c.dirs)
+        assert info.seed_hi - info.seed_lo == len(ent)
+        res = pdist.gather_to_root(off_g[:-1], verts, ent, info)
+        if rank == 0:
+            off, v, e = res
+            np.savez(out_path, offsets=off, verts=v, entered=e, counts=info.counts)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("name", ["trace_sparse48", "trace_curly40_cap"])
+def test_two_rank_concatenation_is_byte_identical(tmp_path, name, oracle_c):
+    path = os.path.join(GOLDEN, f"{name}.npz")
+    out = str(tmp_path / "out.npz")
+    mp.start_processes(_worker, args=(2, _free_port(), path, out), nprocs=2, join=True,
+                       start_method="spawn")
+    got = np.load(out)
+    c = load_case(path)
+    if name == "trace_curly40_cap":
+        # this fixture was traced with its cap plane; the workers trace without it, so
+        # compare against a single-process oracle run under the same inputs instead
+        slab, keep, ent = oracle_c.trace(c.origin, c.voxel_size, c.occ, c.ori, c.seeds, c.dirs,
+                                         c.params)
+        off, v = oracle_c.to_csr(slab, keep)
+    else:
+        off, v, ent = c.offsets, c.verts, c.entered
+    assert np.array_equal(got["offsets"], off)
+    assert np.array_equal(got["verts"], v)
+    assert np.array_equal(got["entered"], ent)
+    assert got["counts"].shape == (2, 2) and got["counts"][:, 0].sum() == len(ent)
+
+
+def test_slice_bounds_match_reference_pool_split():
+    from paper_2604_05794_b200.dist import slice_bounds
+
+    for n, w in ((10, 3), (1_000_000, 8), (7, 8), (0, 2)):
+        assert np.array_equal(slice_bounds(n, w), np.linspace(0, n, w + 1).astype(int))
