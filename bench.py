@@ -211,6 +211,7 @@ def run_ours(args):
     import torch
     import torch.distributed as dist
 
+    from paper_2604_05794_b200 import dist as pdist
     from paper_2604_05794_b200 import phg, synth
     from paper_2604_05794_b200.volume import DeviceField
 
@@ -245,10 +246,8 @@ def run_ours(args):
     def step():
         off, verts, ent = phg.trace_device(field, s_dev, d_dev, params, tracer=tracer,
                                            stream=stream)
-        if ws > 1:
-            mine = torch.tensor([per_rank, int(verts.shape[0])], dtype=torch.int64, device=dev)
-            allc = [torch.empty_like(mine) for _ in range(ws)]
-            dist.all_gather(allc, mine)
+        if ws > 1:  # the one collective: global CSR placement of this rank's strands
+            pdist.exchange_counts(per_rank, int(verts.shape[0]), device=dev)
         return off, verts
 
     if args.sweep:

@@ -111,6 +111,10 @@ phg_status phg_last_kernel_ms(phg_ctx* c, float* trace_ms, float* total_ms);
 /* name of the trace-kernel variant the last trace used (env PHG_VARIANT=<index> selects one;
  * all variants are bit-identical) and the number of compiled variants */
 const char* phg_last_variant(phg_ctx* c);
+/* device self-test of the arithmetic building blocks: runs n randomized and edge-case
+ * operand pairs through the kernel's shared-reciprocal division and the compiler's own
+ * IEEE division and reports how many results differ bitwise (must be 0) */
+phg_status phg_selftest(int64_t n, uint64_t seed, int64_t* mismatches, void* stream);
 int phg_num_variants(void);
 
 #ifdef __cplusplus

@@ -253,3 +253,15 @@ def test_device_api_matches_host_api(gpu):
     assert np.array_equal(o2.cpu().numpy(), off)
     assert np.array_equal(v2.cpu().numpy(), v)
     assert np.array_equal(e2.cpu().numpy().astype(bool), e)
+
+
+def test_shared_reciprocal_division_matches_ieee_division(gpu):
+    """csrc div_by(x, d, div_recip(d)) == x / d bitwise over 8M random + edge operands."""
+    import ctypes
+
+    from paper_2604_05794_b200 import _native
+
+    lib = _native.load()
+    bad = ctypes.c_int64(-1)
+    _native.check(lib.phg_selftest(8_000_000, 12345, ctypes.byref(bad), None), "selftest")
+    assert bad.value == 0
