@@ -231,10 +231,10 @@ def run_ours(args):
     ori_host = occ_host = None
     if rank == 0 and not args.no_cpu:
         ori_host, occ_host = ori.cpu().numpy(), occ.cpu().numpy()
+    all_seeds, all_dirs = synth.config_seeds(cfg, per_rank * ws, ori, occ)
     del ori, occ
     torch.cuda.empty_cache()
 
-    all_seeds, all_dirs = synth.disk_seeds(cfg.n, per_rank * ws, cfg.key)
     s_host = np.ascontiguousarray(all_seeds[rank * per_rank:(rank + 1) * per_rank])
     d_host = np.ascontiguousarray(all_dirs[rank * per_rank:(rank + 1) * per_rank])
     s_dev = torch.from_numpy(s_host).to(dev)

@@ -99,6 +99,31 @@ phg_status phg_gather(phg_ctx* c, double* verts, int64_t verts_cap, void* stream
  * steps (n) int64 = integration steps each strand accepted (vertices appended). */
 phg_status phg_last_steps(phg_ctx* c, int64_t* total_steps);
 
+/* ---- device batch driver (replaces init_guide_strands, phg.py:210-260, with
+ * _trace_field_seeds, phg.py:263-303) ---------------------------------------------------- */
+typedef struct {
+    int32_t batch_size;    /* PhgParams.batch_size: seeds per deferred-commit batch */
+    int32_t occupancy_cap; /* PhgParams.occupancy_cap: at_cap = counts >= cap (phg.py:236) */
+    int32_t field_seeds;   /* PhgParams.field_seeds: 0 disables the field pass */
+    int32_t reserved;
+} phg_grow_params_v1;
+
+/* Scalp seeds/normals (n,3) f64 (scalp.seeds / scalp.seed_normals); counts: (nx,ny,nz)
+ * uint16 vol.counts, read and updated in place exactly as the reference updates it.  The
+ * segments stay on the context: *n_segments strands, *n_verts vertices.  report =
+ * {n_never_entered, n_scalp_segments, n_field_seeds_traced, n_field_segments}.
+ * The field's cap plane is consumed (cleared on return). */
+phg_status phg_grow_init(phg_ctx* c, phg_field* f, const phg_params_v1* p,
+                         const phg_grow_params_v1* g, const double* seeds, const double* normals,
+                         int64_t n, uint16_t* counts, int64_t* n_segments, int64_t* n_verts,
+                         int64_t report[4], void* stream);
+/* Segments of the last phg_grow_init in order (scalp segments in seed order, then field
+ * segments): offsets (n_segments+1) i64, verts (n_verts,3) f64, rooted (n_segments) u8
+ * (1 = Strand(rooted=True, source="traced"), 0 = Strand(rooted=False, source="field")).
+ * Any pointer may be NULL (skipped); host or device memory. */
+phg_status phg_grow_fetch(phg_ctx* c, int64_t* offsets, double* verts, uint8_t* rooted,
+                          void* stream);
+
 /* ---- sampler (replaces sample_orientation_batch, volume.py:183-224) --------- */
 phg_status phg_sample(const phg_field* f, const double* pts, const double* prev, int64_t n,
                       double* dirs, uint8_t* has, double* support, void* stream);

@@ -25,7 +25,7 @@ EXPORTS = (
     "phg_field_create", "phg_field_set_cap", "phg_field_set_near", "phg_field_destroy",
     "phg_field_info", "phg_ctx_create", "phg_ctx_destroy", "phg_trace", "phg_gather",
     "phg_last_steps", "phg_sample", "phg_last_error", "phg_abi_version", "phg_last_kernel_ms",
-    "phg_last_variant", "phg_num_variants", "phg_selftest",
+    "phg_last_variant", "phg_num_variants", "phg_selftest", "phg_grow_init", "phg_grow_fetch",
 )
 
 
@@ -73,6 +73,9 @@ def _declare(lib):
         "phg_last_variant": (ctypes.c_char_p, [VP]),
         "phg_num_variants": (ctypes.c_int, []),
         "phg_selftest": (S, [I64, ctypes.c_uint64, ctypes.POINTER(I64), VP]),
+        "phg_grow_init": (S, [VP, VP, ctypes.POINTER(Params), VP, VP, VP, I64, VP,
+                              ctypes.POINTER(I64), ctypes.POINTER(I64), ctypes.POINTER(I64), VP]),
+        "phg_grow_fetch": (S, [VP, VP, VP, VP, VP]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

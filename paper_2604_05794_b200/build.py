@@ -13,7 +13,8 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
-SRC = os.path.join(HERE, "csrc", "phg_trace.cu")
+SRCS = [os.path.join(HERE, "csrc", f) for f in ("phg_trace.cu", "phg_grow.cu")]
+HDRS = [os.path.join(HERE, "csrc", "phg_core.cuh")]
 OUT = os.path.join(HERE, "libphg_b200.so")
 
 NVCC_FLAGS = [
@@ -30,11 +31,11 @@ def nvcc():
 
 
 def build(force=False, verbose=False):
-    deps = [SRC, os.path.join(ROOT, "include", "phg_b200.h")]
+    deps = SRCS + HDRS + [os.path.join(ROOT, "include", "phg_b200.h")]
     if (not force and os.path.exists(OUT)
             and os.path.getmtime(OUT) >= max(os.path.getmtime(d) for d in deps)):
         return OUT
-    cmd = [nvcc(), *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-o", OUT, SRC]
+    cmd = [nvcc(), *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-o", OUT, *SRCS]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)

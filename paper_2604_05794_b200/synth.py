@@ -136,6 +136,36 @@ def disk_seeds(n_vox: int, count: int, key: int, z_mm: float = 1.3, radius_frac:
     return pos, d
 
 
+def interior_seeds_torch(occ, ori, count: int, key: int):
+    """interior_seeds for (possibly CUDA) torch fields: random occupied voxel centres
+    (with replacement), dir = normalised voxel ori.  Returns float64 numpy arrays."""
+    dev = occ.device
+    g = torch.Generator(device=dev)
+    g.manual_seed(key)
+    idx = torch.nonzero(occ.reshape(-1)).squeeze(1)
+    pick = idx[torch.randint(0, idx.numel(), (count,), generator=g, device=dev)]
+    _, ny, nz = occ.shape
+    ijk = torch.stack([pick // (ny * nz), (pick // nz) % ny, pick % nz], dim=1)
+    pos = (ijk.double() + 0.5) * VOXEL_MM
+    d = ori.reshape(-1, 3)[pick].double()
+    d = d / torch.clamp(torch.linalg.vector_norm(d, dim=1, keepdim=True), min=1e-12)
+    return pos.cpu().numpy(), d.cpu().numpy()
+
+
+def config_seeds(cfg: "Config", count: int, ori=None, occ=None):
+    """Seeds of a bench config: the disk for C1-C4; for the sparse C5 half disk seeds and
+    half interior seeds traced in both directions (+d then -d), as SURVEY.md 8(d) C5."""
+    if cfg.kind != "sparse":
+        return disk_seeds(cfg.n, count, cfg.key)
+    nd = count // 2
+    ni = (count - nd) // 2
+    sd, dd = disk_seeds(cfg.n, nd, cfg.key, radius_frac=0.45)
+    si, di = interior_seeds_torch(occ, ori, ni, cfg.key + 1)
+    pos = np.concatenate([sd, si, si])
+    dirs = np.concatenate([dd, di, -di])
+    return pos, dirs
+
+
 def interior_seeds(occ: np.ndarray, ori: np.ndarray, count: int, key: int):
     """Field-style seeds at centres of random occupied voxels, dir = voxel ori.
 

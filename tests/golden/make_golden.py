@@ -268,29 +268,52 @@ def sampler_case():
     print("sample_sparse24 ok")
 
 
-def driver_case():
+def _driver(name, vol, seeds, dirs, p):
+    scalp = ScalpMesh(vertices=np.zeros((3, 3)), faces=np.zeros((1, 3), int),
+                      vertex_normals=np.zeros((3, 3)), seeds=seeds, seed_normals=dirs)
+    segs, report = phg.init_guide_strands(scalp, vol, p, workers=1)
+    out = [(s.vertices, s.rooted) for s in segs]
+    offsets, verts, rooted = to_csr(out)
+    np.savez_compressed(
+        os.path.join(HERE, f"driver_{name}.npz"), origin=vol.origin,
+        voxel_size=np.float64(vol.voxel_size), occ=vol.occ, ori=vol.ori, seeds=seeds, dirs=dirs,
+        params=np.array(params_json(p)), offsets=offsets, verts=verts, rooted=rooted,
+        counts_out=vol.counts, report=np.array(json.dumps(report)))
+    print(f"driver_{name:18s} segments={len(segs)} report={report}")
+
+
+def driver_cases():
     """init_guide_strands with several deferred-commit batches and a field pass."""
     n = 40
     ori, occ = field_np("sparse", n, sparse_sigma=2.0, sparse_key=7)
     vol = vol_of((0, 0, 0), synth.VOXEL_MM, occ, ori)
     seeds, dirs = synth.disk_seeds(n, 1500, 34, radius_frac=0.45)
-    scalp = ScalpMesh(vertices=np.zeros((3, 3)), faces=np.zeros((1, 3), int),
-                      vertex_normals=np.zeros((3, 3)), seeds=seeds, seed_normals=dirs)
-    p = phg.PhgParams(batch_size=256, occupancy_cap=2, field_seeds=600, n_root=1500)
-    segs, report = phg.init_guide_strands(scalp, vol, p, workers=1)
-    out = [(s.vertices, s.rooted) for s in segs]
-    offsets, verts, rooted = to_csr(out)
-    np.savez_compressed(
-        os.path.join(HERE, "driver_sparse40.npz"), origin=vol.origin,
-        voxel_size=np.float64(vol.voxel_size), occ=vol.occ, ori=vol.ori, seeds=seeds, dirs=dirs,
-        params=np.array(params_json(p)), offsets=offsets, verts=verts, rooted=rooted,
-        counts_out=vol.counts, report=np.array(json.dumps(report)))
-    print(f"driver_sparse40 segments={len(segs)} report={report}")
+    _driver("sparse40", vol, seeds, dirs,
+            phg.PhgParams(batch_size=256, occupancy_cap=2, field_seeds=600, n_root=1500))
+    # curly field, cap 1, many batches; field_seeds larger than the unvisited set (no striding)
+    ori, occ = field_np("curly", 32)
+    vol = vol_of((0, 0, 0), synth.VOXEL_MM, occ, ori)
+    seeds, dirs = synth.disk_seeds(32, 800, 35)
+    _driver("curly32_cap1", vol, seeds, dirs,
+            phg.PhgParams(batch_size=100, occupancy_cap=1, field_seeds=100000, max_vertices=120))
+    # strict mode: per-step commits in both passes, no segment commits
+    ori, occ = field_np("sparse", 32, sparse_sigma=2.0, sparse_key=8)
+    vol = vol_of((0, 0, 0), synth.VOXEL_MM, occ, ori)
+    seeds, dirs = synth.disk_seeds(32, 400, 36, radius_frac=0.45)
+    _driver("sparse32_strict", vol, seeds, dirs,
+            phg.PhgParams(batch_size=128, field_seeds=300, strict=True))
+    # steering + a non-power-of-two voxel size and shifted origin
+    ori, occ = field_np("sparse", 32, sparse_sigma=2.0, sparse_key=9)
+    vol = vol_of((-7.5, 3.25, 1.0), 1.7, occ, ori)
+    seeds, dirs = synth.disk_seeds(32, 400, 37, radius_frac=0.45)
+    seeds = (seeds / synth.VOXEL_MM) * 1.7 + vol.origin
+    _driver("sparse32_steer_vs17", vol, seeds, dirs,
+            phg.PhgParams(batch_size=150, occupancy_cap=3, field_seeds=250, steer=0.5,
+                          step_mm=0.85))
 
 
 if __name__ == "__main__":
-    unit_cases()
-    helix_case()
-    analytic_cases()
-    sampler_case()
-    driver_case()
+    only = sys.argv[1:]  # e.g. `driver` to regenerate only the driver fixtures
+    for fn in (unit_cases, helix_case, analytic_cases, sampler_case, driver_cases):
+        if not only or any(o in fn.__name__ for o in only):
+            fn()

@@ -1,0 +1,102 @@
+"""Deferred-commit batch driver (init_guide_strands, phg.py:210-303): oracle pinned to the
+reference's fixtures on CPU; the device driver (csrc/phg_grow.cu) checked bit-exact on GPU."""
+
+import glob
+import json
+import os
+from types import SimpleNamespace
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, load_case
+
+DRIVER_CASES = sorted(glob.glob(os.path.join(GOLDEN, "driver_*.npz")))
+
+
+def near_map(occ):
+    from scipy.ndimage import distance_transform_edt
+
+    _, inds = distance_transform_edt(~occ, return_indices=True)
+    return np.stack(inds, axis=-1)
+
+
+def _csr(out):
+    off = np.zeros(len(out) + 1, np.int64)
+    off[1:] = np.cumsum([len(v) for v, _ in out])
+    verts = np.concatenate([v for v, _ in out]) if out else np.zeros((0, 3))
+    return off, verts, np.array([r for _, r in out], bool)
+
+
+def test_driver_fixtures_present():
+    assert len(DRIVER_CASES) >= 4
+
+
+@pytest.mark.parametrize("path", DRIVER_CASES, ids=lambda p: os.path.basename(p)[7:-4])
+def test_driver_oracle_matches_reference(path, oracle_c):
+    from oracle import phg_driver_np as dn
+
+    c = load_case(path)
+    counts = np.zeros(c.occ.shape, np.uint16)
+    near = near_map(c.occ) if c.params.steer > 0 else None
+    out, rep = dn.init_guide(c.origin, float(c.voxel_size), c.occ, c.ori, counts, c.seeds, c.dirs,
+                             c.params, near_occ=near)
+    off, verts, rooted = _csr(out)
+    assert np.array_equal(off, c.offsets)
+    assert np.array_equal(verts, c.verts)
+    assert np.array_equal(rooted, c.rooted)
+    assert np.array_equal(counts, c.counts_out)
+    assert rep == json.loads(str(c.report))
+
+
+# ---- GPU ----------------------------------------------------------------------------------
+def _params(d):
+    from paper_2604_05794_b200.phg import PhgParams
+
+    return PhgParams(**{k: d[k] for k in d if k in PhgParams.__dataclass_fields__})
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("path", DRIVER_CASES, ids=lambda p: os.path.basename(p)[7:-4])
+def test_device_driver_matches_reference(path):
+    from paper_2604_05794_b200 import grow
+    from paper_2604_05794_b200.volume import OOVolume
+
+    c = load_case(path)
+    vol = OOVolume.empty(c.origin, float(c.voxel_size), c.occ.shape)
+    vol.occ, vol.ori = c.occ, c.ori
+    scalp = SimpleNamespace(seeds=c.seeds, seed_normals=c.dirs)
+    segs, rep = grow.init_guide_strands(scalp, vol, _params(vars(c.params)))
+    off, verts, rooted = _csr([(s.vertices, s.rooted) for s in segs])
+    assert np.array_equal(off, c.offsets)
+    assert np.array_equal(verts, c.verts)
+    assert np.array_equal(rooted, c.rooted)
+    assert [s.source for s in segs] == ["traced" if r else "field" for r in c.rooted]
+    assert np.array_equal(vol.counts, c.counts_out)
+    assert rep == json.loads(str(c.report))
+
+
+@pytest.mark.gpu
+def test_device_driver_matches_oracle_at_scale(oracle_c):
+    """128^3 curly field, 20k scalp seeds in 5 batches with cap 4, 8k field seeds."""
+    from oracle import phg_driver_np as dn
+    from paper_2604_05794_b200 import grow, synth
+    from paper_2604_05794_b200.volume import OOVolume
+
+    ori, occ = synth.make_field("curly", 128, "cpu")
+    ori, occ = ori.numpy(), occ.numpy()
+    seeds, dirs = synth.disk_seeds(128, 20_000, 41)
+    params = _params(dict(batch_size=4096, occupancy_cap=4, field_seeds=8000, max_vertices=200))
+    vol = OOVolume.empty((0, 0, 0), synth.VOXEL_MM, occ.shape)
+    vol.occ, vol.ori = occ, ori
+    segs, rep = grow.init_guide_strands(SimpleNamespace(seeds=seeds, seed_normals=dirs), vol,
+                                        params)
+    counts = np.zeros(occ.shape, np.uint16)
+    out, rep_o = dn.init_guide(np.zeros(3), synth.VOXEL_MM, occ, ori, counts, seeds, dirs, params)
+    assert rep == rep_o
+    assert np.array_equal(vol.counts, counts)
+    off, verts, rooted = _csr([(s.vertices, s.rooted) for s in segs])
+    off_o, verts_o, rooted_o = _csr(out)
+    assert np.array_equal(off, off_o) and np.array_equal(rooted, rooted_o)
+    assert np.array_equal(verts, verts_o)
+    assert rep["n_scalp_segments"] > 1000 and rep["n_segments"] > rep["n_scalp_segments"]
