@@ -95,6 +95,18 @@ phg_status phg_trace(phg_ctx* c, const phg_field* f, const phg_params_v1* p,
  * (n_verts,3) float64 CSR payload.  verts_cap is in vertices. Blocks when verts is host memory. */
 phg_status phg_gather(phg_ctx* c, double* verts, int64_t verts_cap, void* stream);
 
+/* End-to-end variant of phg_trace + phg_gather for HOST seeds and HOST outputs: seeds are
+ * traced in chunks of `chunk` (<= 0: n/4, at least 65536) and the D2H copy of chunk k's
+ * vertices (on an internal copy stream) overlaps the device work of chunk k+1.  offsets
+ * (n+1) i64, entered (n) u8, verts (verts_cap,3) f64: pinned host memory gives the overlap.
+ * Relaxed mode only (strict mode couples all seeds per step).  If the vertices exceed
+ * verts_cap, returns PHG_ERR_CAPACITY with the required count in *n_verts_out (offsets and
+ * entered are still written). */
+phg_status phg_trace_to_host(phg_ctx* c, const phg_field* f, const phg_params_v1* p,
+                             const double* seed_pos, const double* seed_dir, int64_t n,
+                             int64_t chunk, int64_t* offsets, uint8_t* entered, double* verts,
+                             int64_t verts_cap, int64_t* n_verts_out, void* stream);
+
 /* Per-strand raw counters of the last trace (diagnostics / step accounting):
  * steps (n) int64 = integration steps each strand accepted (vertices appended). */
 phg_status phg_last_steps(phg_ctx* c, int64_t* total_steps);

@@ -26,6 +26,7 @@ EXPORTS = (
     "phg_field_info", "phg_ctx_create", "phg_ctx_destroy", "phg_trace", "phg_gather",
     "phg_last_steps", "phg_sample", "phg_last_error", "phg_abi_version", "phg_last_kernel_ms",
     "phg_last_variant", "phg_num_variants", "phg_selftest", "phg_grow_init", "phg_grow_fetch",
+    "phg_trace_to_host",
 )
 
 
@@ -64,6 +65,8 @@ def _declare(lib):
         "phg_trace": (S, [VP, VP, ctypes.POINTER(Params), VP, VP, I64, VP, VP, VP,
                           ctypes.POINTER(I64), VP]),
         "phg_gather": (S, [VP, VP, I64, VP]),
+        "phg_trace_to_host": (S, [VP, VP, ctypes.POINTER(Params), VP, VP, I64, I64, VP, VP, VP,
+                                  I64, ctypes.POINTER(I64), VP]),
         "phg_last_steps": (S, [VP, ctypes.POINTER(I64)]),
         "phg_sample": (S, [VP, VP, VP, I64, VP, VP, VP, VP]),
         "phg_last_error": (ctypes.c_char_p, []),

@@ -91,6 +91,18 @@ class Tracer:
                                           ctypes.byref(total), stream), "phg_trace")
         return int(total.value)
 
+    def trace_to_host(self, field, params, seed_pos, seed_dir, n, offsets_ptr, entered_ptr,
+                      verts_ptr, verts_cap, chunk=0, stream=0):
+        """phg_trace_to_host: host seeds -> host CSR, D2H overlapped with the next chunk."""
+        p = _native.params_struct(params)
+        total = ctypes.c_int64()
+        _native.check(self._lib.phg_trace_to_host(self.handle, field.handle, ctypes.byref(p),
+                                                  seed_pos, seed_dir, n, chunk, offsets_ptr,
+                                                  entered_ptr, verts_ptr, verts_cap,
+                                                  ctypes.byref(total), stream),
+                      "phg_trace_to_host")
+        return int(total.value)
+
     def gather(self, verts_ptr, cap, stream=0):
         _native.check(self._lib.phg_gather(self.handle, verts_ptr, cap, stream), "phg_gather")
 

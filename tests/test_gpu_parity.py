@@ -255,6 +255,34 @@ def test_device_api_matches_host_api(gpu):
     assert np.array_equal(e2.cpu().numpy().astype(bool), e)
 
 
+def test_pipelined_host_path_matches(gpu):
+    """phg_trace_to_host (chunked, overlapped D2H) == phg_trace + phg_gather, any chunking."""
+    torch = gpu.torch
+    vol, s, d, p = _config_case("sparse", 64, 9_000, 19, interior=2_000)
+    off, v, e = gpu.phg.trace_batch_csr(vol, s, d, p)
+    f = gpu.volume.field_for(vol)
+    f.set_cap(None)
+    f.set_near(None)
+    tr = gpu.phg.Tracer()
+    n = len(s)
+    for chunk in (0, 1000, 4096, n):
+        o2 = torch.empty(n + 1, dtype=torch.int64).pin_memory()
+        e2 = torch.empty(n, dtype=torch.uint8).pin_memory()
+        v2 = torch.empty((len(v) + 5, 3), dtype=torch.float64).pin_memory()
+        total = tr.trace_to_host(f, p, s.ctypes.data, d.ctypes.data, n, o2.data_ptr(),
+                                 e2.data_ptr(), v2.data_ptr(), v2.shape[0], chunk)
+        assert total == len(v)
+        assert np.array_equal(o2.numpy(), off)
+        assert np.array_equal(e2.numpy().astype(bool), e)
+        assert np.array_equal(v2.numpy()[:total], v)
+    from paper_2604_05794_b200.errors import PipelineError
+
+    small = torch.empty((10, 3), dtype=torch.float64).pin_memory()
+    with pytest.raises(PipelineError):
+        tr.trace_to_host(f, p, s.ctypes.data, d.ctypes.data, n, o2.data_ptr(), e2.data_ptr(),
+                         small.data_ptr(), 10, 0)
+
+
 def test_shared_reciprocal_division_matches_ieee_division(gpu):
     """csrc div_by(x, d, div_recip(d)) == x / d bitwise over 8M random + edge operands."""
     import ctypes
