@@ -45,6 +45,7 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=0, help="seeds in the CPU sample")
     ap.add_argument("--sweep", action="store_true", help="time every trace-kernel variant")
+    ap.add_argument("--no-driver", action="store_true", help="skip the batch-driver leg")
     return ap.parse_args()
 
 
@@ -293,6 +294,10 @@ def run_ours(args):
     if not args.no_e2e:
         e2e = e2e_leg(args, tracer, field, params, s_host, d_host, per_rank, ws, dev, steps_per_trace)
 
+    driver = None
+    if not args.no_driver and ws == 1:
+        driver = driver_leg(cfg, field, s_host, d_host, dev)
+
     kernel_ms = float(np.mean(kern_ms))
     peak, peak_kind = measured_peak()
     achieved = accepted * BYTES_PER_STEP / (kernel_ms / 1e3) / 1e9
@@ -332,12 +337,56 @@ def run_ours(args):
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": "trace_kernel", "kernel_ms": kernel_ms,
                          "bytes_per_step": BYTES_PER_STEP, "peak_source": peak_kind},
-            "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
+            "cpu_baseline": cpu, "e2e": e2e, "clocks": clk, "driver": driver,
             "gpu_launches": args.steps * phg.LAUNCHES_PER_TRACE,
         }
         print(json.dumps(line), flush=True)
     if ws > 1:
         dist.destroy_process_group()
+
+
+def driver_leg(cfg, field, s_host, d_host, dev, repeats=2):
+    """init_guide_strands on the device (csrc/phg_grow.cu) with the reference's defaults:
+    deferred-commit batches of 16384 seeds, occupancy_cap 16, 30000 field seeds; host seeds
+    in, host CSR + updated counts out (wall clock, includes all copies)."""
+    import ctypes
+
+    import torch
+
+    from paper_2604_05794_b200 import _native, grow
+    from paper_2604_05794_b200.phg import PhgParams, _tracer
+
+    params = PhgParams()
+    lib = _native.load()
+    tr = _tracer()
+    counts = np.zeros(field.dims, np.uint16)
+    p = _native.params_struct(params)
+    g = grow.GrowParams(params.batch_size, params.occupancy_cap, params.field_seeds, 0)
+    nseg, nv = ctypes.c_int64(), ctypes.c_int64()
+    rep = (ctypes.c_int64 * 4)()
+    times = []
+    for _ in range(repeats):
+        counts[:] = 0
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        _native.check(lib.phg_grow_init(tr.handle, field.handle, ctypes.byref(p), ctypes.byref(g),
+                                        s_host.ctypes.data, d_host.ctypes.data, len(s_host),
+                                        counts.ctypes.data, ctypes.byref(nseg), ctypes.byref(nv),
+                                        rep, None), "phg_grow_init")
+        offsets = np.empty(nseg.value + 1, np.int64)
+        verts = np.empty((nv.value, 3))
+        rooted = np.empty(nseg.value, np.uint8)
+        _native.check(lib.phg_grow_fetch(tr.handle, offsets.ctypes.data, verts.ctypes.data,
+                                         rooted.ctypes.data, None), "phg_grow_fetch")
+        times.append(time.perf_counter() - t0)
+    t = min(times)
+    steps = int(nv.value - nseg.value)
+    return {"what": "init_guide_strands (phg.py:210-303) on device, reference defaults",
+            "seeds": int(len(s_host)), "batch_size": params.batch_size,
+            "batches": int((len(s_host) + params.batch_size - 1) // params.batch_size),
+            "field_seeds_traced": int(rep[2]), "segments": int(nseg.value),
+            "scalp_segments": int(rep[1]), "vertices": int(nv.value), "seconds": t,
+            "segment_steps_per_s": steps / t, "all_times_s": times}
 
 
 def sweep_variants(args, step, tracer, flush):
