@@ -364,7 +364,7 @@ def driver_leg(cfg, field, s_host, d_host, dev, repeats=2):
     g = grow.GrowParams(params.batch_size, params.occupancy_cap, params.field_seeds, 0)
     nseg, nv = ctypes.c_int64(), ctypes.c_int64()
     rep = (ctypes.c_int64 * 4)()
-    times = []
+    times, dev_ms = [], []
     for _ in range(repeats):
         counts[:] = 0
         torch.cuda.synchronize()
@@ -379,6 +379,7 @@ def driver_leg(cfg, field, s_host, d_host, dev, repeats=2):
         _native.check(lib.phg_grow_fetch(tr.handle, offsets.ctypes.data, verts.ctypes.data,
                                          rooted.ctypes.data, None), "phg_grow_fetch")
         times.append(time.perf_counter() - t0)
+        dev_ms.append(tr.last_kernel_ms()[1])
     t = min(times)
     steps = int(nv.value - nseg.value)
     return {"what": "init_guide_strands (phg.py:210-303) on device, reference defaults",
@@ -386,7 +387,10 @@ def driver_leg(cfg, field, s_host, d_host, dev, repeats=2):
             "batches": int((len(s_host) + params.batch_size - 1) // params.batch_size),
             "field_seeds_traced": int(rep[2]), "segments": int(nseg.value),
             "scalp_segments": int(rep[1]), "vertices": int(nv.value), "seconds": t,
-            "segment_steps_per_s": steps / t, "all_times_s": times}
+            "segment_steps_per_s": steps / t, "all_times_s": times,
+            "device_ms": min(dev_ms),
+            "note": "seconds = wall clock incl. vol.counts H2D/D2H and the pageable host CSR "
+                    "copy; device_ms = CUDA-event window of the device work alone"}
 
 
 def sweep_variants(args, step, tracer, flush):

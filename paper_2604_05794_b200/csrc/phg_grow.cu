@@ -101,7 +101,8 @@ __device__ __forceinline__ bool set_insert(unsigned long long* T, int bits, uint
 __device__ __forceinline__ void commit_row(const FieldView& F, const double* __restrict__ row,
                                            long long L, unsigned long long* T, int bits,
                                            uint32_t epoch, uint32_t* __restrict__ counts,
-                                           int lane) {
+                                           uint32_t* __restrict__ cap_bits, uint32_t cap,
+                                           unsigned int* __restrict__ wrapped, int lane) {
     for (long long k = lane; k < L; k += 32) {
         // vol.voxel_of (volume.py:42-45) and in_bounds (:47-49)
         const int vx = floor_idx(grid_coord(F, row[3 * k + 0] - F.ox));
@@ -110,7 +111,14 @@ __device__ __forceinline__ void commit_row(const FieldView& F, const double* __r
         if ((unsigned)vx < (unsigned)F.nx && (unsigned)vy < (unsigned)F.ny &&
             (unsigned)vz < (unsigned)F.nz) {
             const uint32_t lin = ((uint32_t)vx * F.ny + vy) * F.nz + vz;
-            if (set_insert(T, bits, epoch, lin)) atomicAdd(counts + lin, 1u);
+            if (set_insert(T, bits, epoch, lin)) {
+                // keep the at_cap plane (counts >= cap, phg.py:236) current incrementally:
+                // without uint16 wrap-around counts only grow, so a voxel turns "at cap"
+                // exactly when its count reaches cap; a wrap forces a full rebuild
+                const uint32_t now = (atomicAdd(counts + lin, 1u) + 1u) & 0xffffu;
+                if (now == cap) atomicOr(cap_bits + (lin >> 5), 1u << (lin & 31));
+                if (now == 0u) atomicOr(wrapped, 1u);
+            }
         }
     }
 }
@@ -124,7 +132,8 @@ __global__ void commit_kernel(FieldView F, const double* __restrict__ slab_a,
                               const double* __restrict__ slab_b,
                               const long long* __restrict__ keep_b,
                               const uint8_t* __restrict__ valid, long long n, size_t row_stride,
-                              uint32_t* __restrict__ counts, int bits,
+                              uint32_t* __restrict__ counts, uint32_t* __restrict__ cap_bits,
+                              uint32_t cap, unsigned int* __restrict__ wrapped, int bits,
                               unsigned long long* __restrict__ gtables) {
     extern __shared__ unsigned long long smem_tables[];
     const int lane = threadIdx.x & 31;
@@ -139,9 +148,10 @@ __global__ void commit_kernel(FieldView F, const double* __restrict__ slab_a,
     for (long long i = gwarp; i < n; i += nwarps) {
         if (!valid[i]) continue;
         ++epoch;
-        commit_row(F, slab_a + (size_t)i * row_stride, keep_a[i], T, bits, epoch, counts, lane);
+        commit_row(F, slab_a + (size_t)i * row_stride, keep_a[i], T, bits, epoch, counts,
+                   cap_bits, cap, wrapped, lane);
         if (slab_b) commit_row(F, slab_b + (size_t)i * row_stride, keep_b[i], T, bits, epoch,
-                               counts, lane);
+                               counts, cap_bits, cap, wrapped, lane);
         __syncwarp();
     }
 }
@@ -316,7 +326,8 @@ struct GrowState {
     uint32_t* counts;    // device uint32 plane (vol.counts)
     long long segs = 0;  // output segments so far
     long long verts = 0; // output vertices so far
-    unsigned long long* misc = nullptr;  // [0] never_entered
+    unsigned long long* misc = nullptr;  // [0] never_entered, [1] (u32) count wrapped
+    bool cap_valid = false;              // f->cap == (counts >= cap) for the current counts
 };
 
 phg_status set_cap_plane(GrowState& S) {
@@ -324,12 +335,14 @@ phg_status set_cap_plane(GrowState& S) {
         S.f->has_cap = false;
         return PHG_OK;
     }
+    S.f->has_cap = true;
+    if (S.cap_valid) return PHG_OK;  // maintained incrementally by the commit kernel
     const long long V = S.f->nvox();
     PHG_TRY(S.f->cap.ensure((size_t)((V + 31) / 32) * 4));
     cap_from_counts_kernel<<<grid_for((V + 31) / 32 * 32, 256, num_sms() * 16), 256, 0, S.st>>>(
         S.counts, V, (uint32_t)S.g->occupancy_cap, S.f->cap.as<uint32_t>());
     PHG_CUDA(cudaGetLastError());
-    S.f->has_cap = true;
+    S.cap_valid = true;
     return PHG_OK;
 }
 
@@ -350,13 +363,15 @@ phg_status launch_commit(GrowState& S, const double* slab_a, const long long* ke
         const int blocks = std::max(1, std::min(warps_total / kCommitWarps,
                                                 (int)((n + kCommitWarps - 1) / kCommitWarps)));
         commit_kernel<false><<<blocks, 32 * kCommitWarps, smem, S.st>>>(
-            F, slab_a, keep_a, slab_b, keep_b, valid, n, rs, S.counts, bits, nullptr);
+            F, slab_a, keep_a, slab_b, keep_b, valid, n, rs, S.counts, S.f->cap.as<uint32_t>(),
+            (uint32_t)S.g->occupancy_cap, (unsigned int*)(S.misc + 1), bits, nullptr);
     } else {
         const int blocks = std::max(1, std::min(warps_total / kCommitWarps,
                                                 (int)((n + kCommitWarps - 1) / kCommitWarps)));
         PHG_TRY(S.c->g_hash.ensure(table_bytes * (size_t)blocks * kCommitWarps));
         commit_kernel<true><<<blocks, 32 * kCommitWarps, 0, S.st>>>(
-            F, slab_a, keep_a, slab_b, keep_b, valid, n, rs, S.counts, bits,
+            F, slab_a, keep_a, slab_b, keep_b, valid, n, rs, S.counts, S.f->cap.as<uint32_t>(),
+            (uint32_t)S.g->occupancy_cap, (unsigned int*)(S.misc + 1), bits,
             S.c->g_hash.as<unsigned long long>());
     }
     PHG_CUDA(cudaGetLastError());
@@ -370,9 +385,14 @@ phg_status batch_offsets(GrowState& S, long long n, long long* lens, long long* 
     PHG_TRY(scan_lengths(S.c, segf, n, sidx, S.st));
     PHG_CUDA(cudaMemcpyAsync(S.c->host_total, voff + n, 8, cudaMemcpyDeviceToHost, S.st));
     PHG_CUDA(cudaMemcpyAsync(S.c->host_total + 1, sidx + n, 8, cudaMemcpyDeviceToHost, S.st));
+    PHG_CUDA(cudaMemcpyAsync(S.c->host_total + 2, S.misc + 1, 8, cudaMemcpyDeviceToHost, S.st));
     PHG_CUDA(cudaStreamSynchronize(S.st));
     *nv = S.c->host_total[0];
     *ns = S.c->host_total[1];
+    if (S.c->host_total[2]) {  // a count wrapped past 65535: rebuild the cap plane exactly
+        S.cap_valid = false;
+        PHG_CUDA(cudaMemsetAsync(S.misc + 1, 0, 8, S.st));
+    }
     return PHG_OK;
 }
 
@@ -582,6 +602,7 @@ phg_status phg_grow_init(phg_ctx* c, phg_field* f, const phg_params_v1* p,
         PHG_TRY(to_device(seeds, (size_t)n * 24, c->g_seeds_pos, &d_pos, st));
         PHG_TRY(to_device(normals, (size_t)n * 24, c->g_seeds_dir, &d_dir, st));
     }
+    PHG_CUDA(cudaEventRecord(c->ev[0], st));  // device window: uploads done .. downloads begin
     phg_status s = PHG_OK;
     if (n > 0) s = scalp_pass(S, (const double*)d_pos, (const double*)d_dir, n);
     long long scalp_segs = S.segs;
@@ -589,6 +610,7 @@ phg_status phg_grow_init(phg_ctx* c, phg_field* f, const phg_params_v1* p,
     if (s == PHG_OK && n > 0 && g->field_seeds > 0) s = field_pass(S, &n_field);
     f->has_cap = false;  // the driver overwrote the field's cap plane; leave none behind
     if (s != PHG_OK) return s;
+    PHG_CUDA(cudaEventRecord(c->ev[2], st));
     // counts back to vol.counts (uint16 wrap like np ndarray +=)
     uint16_t* dst16 = counts_dev ? counts : c->live_stage.as<uint16_t>();
     u32_to_u16<<<grid_for(V, 256, num_sms() * 16), 256, 0, st>>>(S.counts, dst16, V);
@@ -601,6 +623,7 @@ phg_status phg_grow_init(phg_ctx* c, phg_field* f, const phg_params_v1* p,
     PHG_CUDA(cudaMemcpyAsync(c->g_out_off.as<long long>() + S.segs, &S.verts, 8,
                              cudaMemcpyHostToDevice, st));
     PHG_CUDA(cudaStreamSynchronize(st));
+    cudaEventElapsedTime(&c->last_total_ms, c->ev[0], c->ev[2]);
     report[0] = (int64_t)never;
     report[1] = scalp_segs;
     report[2] = n_field;

@@ -77,6 +77,35 @@ def test_device_driver_matches_reference(path):
 
 
 @pytest.mark.gpu
+def test_device_driver_prefilled_counts_and_uint16_wrap(oracle_c):
+    """Pre-filled vol.counts (some at 65535 so commits wrap to 0 like numpy's uint16 +=):
+    the incrementally maintained cap plane must match counts >= cap after every batch."""
+    from oracle import phg_driver_np as dn
+    from paper_2604_05794_b200 import grow, synth
+    from paper_2604_05794_b200.volume import OOVolume
+
+    ori, occ = synth.make_field("curly", 40, "cpu")
+    ori, occ = ori.numpy(), occ.numpy()
+    rng = np.random.Generator(np.random.Philox(key=77))
+    init = rng.choice(np.array([0, 0, 0, 1, 2, 3, 65534, 65535], np.uint16), size=occ.shape)
+    seeds, dirs = synth.disk_seeds(40, 3000, 42)
+    params = _params(dict(batch_size=300, occupancy_cap=3, field_seeds=700, max_vertices=150))
+    vol = OOVolume.empty((0, 0, 0), synth.VOXEL_MM, occ.shape)
+    vol.occ, vol.ori, vol.counts = occ, ori, init.copy()
+    segs, rep = grow.init_guide_strands(SimpleNamespace(seeds=seeds, seed_normals=dirs), vol,
+                                        params)
+    counts = init.copy()
+    out, rep_o = dn.init_guide(np.zeros(3), synth.VOXEL_MM, occ, ori, counts, seeds, dirs, params)
+    assert np.array_equal(vol.counts, counts)
+    assert rep == rep_o
+    off, verts, rooted = _csr([(s.vertices, s.rooted) for s in segs])
+    off_o, verts_o, rooted_o = _csr(out)
+    assert np.array_equal(off, off_o) and np.array_equal(verts, verts_o)
+    assert np.array_equal(rooted, rooted_o)
+    assert (counts < init).any()  # some voxel really wrapped
+
+
+@pytest.mark.gpu
 def test_device_driver_matches_oracle_at_scale(oracle_c):
     """128^3 curly field, 20k scalp seeds in 5 batches with cap 4, 8k field seeds."""
     from oracle import phg_driver_np as dn
