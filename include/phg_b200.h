@@ -136,6 +136,19 @@ phg_status phg_grow_init(phg_ctx* c, phg_field* f, const phg_params_v1* p,
 phg_status phg_grow_fetch(phg_ctx* c, int64_t* offsets, double* verts, uint8_t* rooted,
                           void* stream);
 
+/* ---- wire formats ------------------------------------------------------------------
+ * STND image (write_strands, strands.py:63-69) of a CSR strand set: u32 magic 0x444E5453,
+ * u32 count, per strand u32 n + n*3 float32 (vertices rounded to nearest).  `out` must hold
+ * 8 + 4*n_strands + 12*offsets[n_strands] bytes; host or device pointers. */
+phg_status phg_stnd_encode(const int64_t* offsets, const double* verts, int64_t n_strands,
+                           uint8_t* out, void* stream);
+/* Field straight from an OOVL payload (read_volume, volume.py:248-266): bits =
+ * np.packbits(occ) ((nx*ny*nz+7)/8 bytes, MSB first), ori_occupied = (n_occ,3) float32 of the
+ * occupied voxels in C order.  PHG_ERR_INVALID if n_occ != number of set bits (truncated). */
+phg_status phg_field_from_oovl(phg_field** out, const uint8_t* bits, const float* ori_occupied,
+                               int64_t n_occ, int64_t nx, int64_t ny, int64_t nz,
+                               const double origin[3], double voxel_size, void* stream);
+
 /* ---- sampler (replaces sample_orientation_batch, volume.py:183-224) --------- */
 phg_status phg_sample(const phg_field* f, const double* pts, const double* prev, int64_t n,
                       double* dirs, uint8_t* has, double* support, void* stream);

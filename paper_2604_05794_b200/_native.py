@@ -26,7 +26,7 @@ EXPORTS = (
     "phg_field_info", "phg_ctx_create", "phg_ctx_destroy", "phg_trace", "phg_gather",
     "phg_last_steps", "phg_sample", "phg_last_error", "phg_abi_version", "phg_last_kernel_ms",
     "phg_last_variant", "phg_num_variants", "phg_selftest", "phg_grow_init", "phg_grow_fetch",
-    "phg_trace_to_host",
+    "phg_trace_to_host", "phg_stnd_encode", "phg_field_from_oovl",
 )
 
 
@@ -79,6 +79,9 @@ def _declare(lib):
         "phg_grow_init": (S, [VP, VP, ctypes.POINTER(Params), VP, VP, VP, I64, VP,
                               ctypes.POINTER(I64), ctypes.POINTER(I64), ctypes.POINTER(I64), VP]),
         "phg_grow_fetch": (S, [VP, VP, VP, VP, VP]),
+        "phg_stnd_encode": (S, [VP, VP, I64, VP, VP]),
+        "phg_field_from_oovl": (S, [ctypes.POINTER(VP), VP, VP, I64, I64, I64, I64,
+                                    ctypes.POINTER(ctypes.c_double), ctypes.c_double, VP]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

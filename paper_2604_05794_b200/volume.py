@@ -110,6 +110,19 @@ class DeviceField:
         self._cap_key = None
         self._near_key = None
 
+    @classmethod
+    def from_handle(cls, handle, dims, origin, voxel_size):
+        """Wrap a phg_field* created by another C entry point (e.g. phg_field_from_oovl)."""
+        self = cls.__new__(cls)
+        self.handle = handle
+        self._lib = _native.load()
+        self.dims = tuple(int(d) for d in dims)
+        self.origin = np.ascontiguousarray(np.asarray(origin, dtype=np.float64).reshape(3))
+        self.voxel_size = float(voxel_size)
+        self._cap_key = None
+        self._near_key = None
+        return self
+
     def close(self):
         if self.handle:
             self._lib.phg_field_destroy(self.handle)

@@ -34,6 +34,7 @@ sys.path.insert(0, ROOT)
 
 from strandkit import phg  # noqa: E402
 from strandkit.scalp import ScalpMesh  # noqa: E402
+from strandkit.strands import Strand  # noqa: E402
 from strandkit.volume import OOVolume, sample_orientation_batch  # noqa: E402
 
 from paper_2604_05794_b200 import synth  # noqa: E402
@@ -312,8 +313,23 @@ def driver_cases():
                           step_mm=0.85))
 
 
+def io_cases():
+    """Reference wire formats: STND (strands.py:63-69) and OOVL (volume.py:236-246)."""
+    from strandkit.strands import StrandSet, write_strands
+    from strandkit.volume import write_volume
+
+    z = np.load(os.path.join(HERE, "driver_sparse40.npz"))
+    off, verts = z["offsets"], z["verts"]
+    segs = [Strand(vertices=verts[off[i]:off[i + 1]]) for i in range(len(off) - 1)]
+    write_strands(os.path.join(HERE, "io_driver_sparse40.stnd"), StrandSet(segs))
+    ori, occ = field_np("sparse", 24, sparse_sigma=1.5)
+    vol = vol_of((-5.0, 3.0, 1.0), 1.5, occ, ori)
+    write_volume(os.path.join(HERE, "io_sparse24.oovl"), vol)
+    print("io fixtures written")
+
+
 if __name__ == "__main__":
     only = sys.argv[1:]  # e.g. `driver` to regenerate only the driver fixtures
-    for fn in (unit_cases, helix_case, analytic_cases, sampler_case, driver_cases):
+    for fn in (unit_cases, helix_case, analytic_cases, sampler_case, driver_cases, io_cases):
         if not only or any(o in fn.__name__ for o in only):
             fn()
