@@ -136,6 +136,33 @@ phg_status phg_grow_init(phg_ctx* c, phg_field* f, const phg_params_v1* p,
 phg_status phg_grow_fetch(phg_ctx* c, int64_t* offsets, double* verts, uint8_t* rooted,
                           void* stream);
 
+/* ---- linking + attachment (replaces compute_links / connect_segments, phg.py:337-413,
+ * attach_to_scalp, phg.py:419-439, and the tangents of grow, phg.py:467-468) ------------- */
+typedef struct {
+    double link_dist_mm;     /* PhgParams.link_dist_mm */
+    double link_cos_gate;    /* np.cos(np.deg2rad(link_angle_deg)) computed by the caller */
+    double smooth_strength;  /* PhgParams.smooth_strength */
+    double step_mm;          /* PhgParams.step_mm (resampling step) */
+    double attach_radius_mm; /* PhgParams.attach_radius_mm */
+    int32_t tangent_window;  /* PhgParams.tangent_window */
+    int32_t smooth;          /* PhgParams.smooth */
+    int32_t smooth_iters;    /* PhgParams.smooth_iters */
+    int32_t attach;          /* 1: attach_to_scalp with the given scalp vertices; 0: skip */
+} phg_link_params_v1;
+
+/* Segments as CSR (offsets (n+1) i64, verts f64, rooted u8, source u8 with 0 traced, 1 field,
+ * 2 linked, 3 attached) -- or offsets == NULL to take the last phg_grow_init result of the
+ * context.  scalp: (n_scalp,3) f64 scalp.vertices (attach only).  Results stay on the context;
+ * counts_out = {n_strands, n_verts, n_links, n_unrooted}. */
+phg_status phg_link(phg_ctx* c, const int64_t* offsets, const double* verts,
+                    const uint8_t* rooted, const uint8_t* source, int64_t n,
+                    const double* scalp, int64_t n_scalp, const phg_link_params_v1* lp,
+                    int64_t counts_out[4], void* stream);
+/* Strands of the last phg_link: offsets (n_strands+1), verts / tangents (n_verts,3) f64,
+ * rooted / source (n_strands) u8, links (n_links,2) i64 in acceptance order.  NULL skips. */
+phg_status phg_link_fetch(phg_ctx* c, int64_t* offsets, double* verts, double* tangents,
+                          uint8_t* rooted, uint8_t* source, int64_t* links, void* stream);
+
 /* ---- wire formats ------------------------------------------------------------------
  * STND image (write_strands, strands.py:63-69) of a CSR strand set: u32 magic 0x444E5453,
  * u32 count, per strand u32 n + n*3 float32 (vertices rounded to nearest).  `out` must hold

@@ -26,8 +26,18 @@ EXPORTS = (
     "phg_field_info", "phg_ctx_create", "phg_ctx_destroy", "phg_trace", "phg_gather",
     "phg_last_steps", "phg_sample", "phg_last_error", "phg_abi_version", "phg_last_kernel_ms",
     "phg_last_variant", "phg_num_variants", "phg_selftest", "phg_grow_init", "phg_grow_fetch",
-    "phg_trace_to_host", "phg_stnd_encode", "phg_field_from_oovl",
+    "phg_trace_to_host", "phg_stnd_encode", "phg_field_from_oovl", "phg_link", "phg_link_fetch",
 )
+
+
+class LinkParams(ctypes.Structure):
+    """phg_link_params_v1"""
+
+    _fields_ = [("link_dist_mm", ctypes.c_double), ("link_cos_gate", ctypes.c_double),
+                ("smooth_strength", ctypes.c_double), ("step_mm", ctypes.c_double),
+                ("attach_radius_mm", ctypes.c_double), ("tangent_window", ctypes.c_int32),
+                ("smooth", ctypes.c_int32), ("smooth_iters", ctypes.c_int32),
+                ("attach", ctypes.c_int32)]
 
 
 class Params(ctypes.Structure):
@@ -80,6 +90,9 @@ def _declare(lib):
                               ctypes.POINTER(I64), ctypes.POINTER(I64), ctypes.POINTER(I64), VP]),
         "phg_grow_fetch": (S, [VP, VP, VP, VP, VP]),
         "phg_stnd_encode": (S, [VP, VP, I64, VP, VP]),
+        "phg_link": (S, [VP, VP, VP, VP, VP, I64, VP, I64, ctypes.POINTER(LinkParams),
+                         ctypes.POINTER(I64), VP]),
+        "phg_link_fetch": (S, [VP, VP, VP, VP, VP, VP, VP, VP]),
         "phg_field_from_oovl": (S, [ctypes.POINTER(VP), VP, VP, I64, I64, I64, I64,
                                     ctypes.POINTER(ctypes.c_double), ctypes.c_double, VP]),
     }

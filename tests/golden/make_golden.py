@@ -313,6 +313,74 @@ def driver_cases():
                           step_mm=0.85))
 
 
+def _strands_npz(path, strands, **extra):
+    src_code = {"traced": 0, "field": 1, "linked": 2, "attached": 3}
+    off = np.zeros(len(strands) + 1, np.int64)
+    off[1:] = np.cumsum([len(s.vertices) for s in strands])
+    verts = np.concatenate([s.vertices for s in strands]) if strands else np.zeros((0, 3))
+    tang = (np.concatenate([s.tangents for s in strands])
+            if strands and strands[0].tangents is not None else np.zeros((0, 3)))
+    np.savez_compressed(path, offsets=off, verts=verts, tangents=tang,
+                        rooted=np.array([s.rooted for s in strands], bool),
+                        source=np.array([src_code[s.source] for s in strands], np.uint8), **extra)
+
+
+def link_cases():
+    """compute_links / connect_segments (phg.py:337-413), attach_to_scalp (:419-439), grow (:445)."""
+    rng = np.random.Generator(np.random.Philox(key=62))
+    # the reference's own random-segment linking setup (test_phg.py:130-179)
+    segs = []
+    for _ in range(400):
+        a = rng.uniform(-60.0, 60.0, 3)
+        d = rng.normal(size=3)
+        d /= np.linalg.norm(d)
+        k = int(rng.integers(3, 7))
+        segs.append(Strand(vertices=a + np.outer(np.linspace(0, 6.0, k), d)))
+    p = phg.PhgParams(link_dist_mm=8.0, link_angle_deg=45.0)
+    links = np.array(phg.compute_links(segs, p), np.int64).reshape(-1, 2)
+    seg_off = np.zeros(len(segs) + 1, np.int64)
+    seg_off[1:] = np.cumsum([len(s.vertices) for s in segs])
+    strands = phg.connect_segments(segs, p)
+    _strands_npz(os.path.join(HERE, "link_random400.npz"), strands, links=links,
+                 seg_offsets=seg_off, seg_verts=np.concatenate([s.vertices for s in segs]),
+                 seg_rooted=np.zeros(len(segs), bool), seg_source=np.zeros(len(segs), np.uint8),
+                 params=np.array(json.dumps({"link_dist_mm": 8.0, "link_angle_deg": 45.0,
+                                             "tangent_window": 3, "smooth": True,
+                                             "smooth_strength": 0.25, "smooth_iters": 2,
+                                             "step_mm": 1.0})))
+    print(f"link_random400 links={len(links)} strands={len(strands)}")
+    # full grow() on driver scenes, with a planar scalp grid under the seeds
+    for name, n, kind, kw, nseeds, key, pkw in (
+            ("sparse40", 40, "sparse", dict(sparse_sigma=2.0, sparse_key=7), 1500, 34,
+             dict(batch_size=256, occupancy_cap=2, field_seeds=600)),
+            ("curly32", 32, "curly", {}, 800, 35,
+             dict(batch_size=100, occupancy_cap=1, field_seeds=100000, max_vertices=120,
+                  link_dist_mm=3.0, link_angle_deg=60.0))):
+        ori, occ = field_np(kind, n, **kw)
+        vol = vol_of((0, 0, 0), synth.VOXEL_MM, occ, ori)
+        seeds, dirs = synth.disk_seeds(n, nseeds, key, radius_frac=0.45)
+        L = n * synth.VOXEL_MM
+        g = np.arange(1.0, L, 2.0)
+        gx, gy = np.meshgrid(g, g, indexing="ij")
+        keep = (gx - L / 2) ** 2 + (gy - L / 2) ** 2 < (0.47 * L) ** 2
+        sv = np.stack([gx[keep], gy[keep], np.full(keep.sum(), 0.5)], axis=1)
+        scalp = ScalpMesh(vertices=sv, faces=np.zeros((1, 3), int),
+                          vertex_normals=np.tile([0.0, 0.0, 1.0], (len(sv), 1)), seeds=seeds,
+                          seed_normals=dirs)
+        p = phg.PhgParams(**pkw)
+        sset, report = phg.grow(scalp, vol, p, workers=1)
+        rep = {k: v for k, v in report.items() if not k.startswith("t_")}
+        _strands_npz(os.path.join(HERE, f"grow_{name}.npz"), sset.strands, origin=vol.origin,
+                     voxel_size=np.float64(vol.voxel_size), occ=vol.occ, ori=vol.ori,
+                     seeds=seeds, dirs=dirs, scalp_vertices=sv,
+                     params=np.array(params_json(p)),
+                     link_params=np.array(json.dumps({k: getattr(p, k) for k in (
+                         "link_dist_mm", "link_angle_deg", "tangent_window", "smooth",
+                         "smooth_strength", "smooth_iters", "step_mm", "attach_radius_mm")})),
+                     report=np.array(json.dumps(rep)))
+        print(f"grow_{name} strands={len(sset)} report={rep}")
+
+
 def io_cases():
     """Reference wire formats: STND (strands.py:63-69) and OOVL (volume.py:236-246)."""
     from strandkit.strands import StrandSet, write_strands
@@ -330,6 +398,7 @@ def io_cases():
 
 if __name__ == "__main__":
     only = sys.argv[1:]  # e.g. `driver` to regenerate only the driver fixtures
-    for fn in (unit_cases, helix_case, analytic_cases, sampler_case, driver_cases, io_cases):
+    for fn in (unit_cases, helix_case, analytic_cases, sampler_case, driver_cases, io_cases,
+               link_cases):
         if not only or any(o in fn.__name__ for o in only):
             fn()
