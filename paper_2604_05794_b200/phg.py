@@ -227,22 +227,36 @@ def trace_device(field, seed_pos, seed_dir, params, tracer=None, stream=None, or
 _SAVED = {}
 
 
-def install(module=None):
+_REROUTED = ("trace_batch", "_make_pool", "init_guide_strands", "connect_segments", "grow")
+
+
+def install(module=None, full=False):
     """Reroute the reference grow stage through the GPU.
 
-    Replaces ``strandkit.phg.trace_batch`` (resolved as a module global by
+    Always replaces ``strandkit.phg.trace_batch`` (resolved as a module global by
     every caller) and disables the fork pool (``_make_pool`` -> None,
     phg.py:184-196) because CUDA state must not be inherited by forked workers;
     the batch loop then calls trace_batch in-process (phg.py:239-241).
+    ``full=True`` also replaces ``init_guide_strands`` (device batch driver,
+    grow.py), ``connect_segments`` and ``grow`` (link.py), so the whole PHG stage
+    -- tracing, deferred commits, field seeds, linking, attachment, tangents --
+    runs on the GPU.
     """
     if module is None:
         import strandkit.phg as module  # type: ignore
     if module in _SAVED:
         return module
-    _SAVED[module] = (module.trace_batch, getattr(module, "_make_pool", None))
+    _SAVED[module] = {k: getattr(module, k) for k in _REROUTED if hasattr(module, k)}
     module.trace_batch = trace_batch
     if hasattr(module, "_make_pool"):
         module._make_pool = lambda *a, **k: None
+    if full:
+        from . import grow as _grow
+        from . import link as _link
+
+        module.init_guide_strands = _grow.init_guide_strands
+        module.connect_segments = _link.connect_segments
+        module.grow = _link.grow
     return module
 
 
@@ -250,7 +264,5 @@ def uninstall(module=None):
     if module is None:
         import strandkit.phg as module  # type: ignore
     saved = _SAVED.pop(module, None)
-    if saved:
-        module.trace_batch = saved[0]
-        if saved[1] is not None:
-            module._make_pool = saved[1]
+    for k, v in (saved or {}).items():
+        setattr(module, k, v)

@@ -239,6 +239,17 @@ def test_install_reroutes_module_global(gpu):
     finally:
         gpu.phg.uninstall(mod)
     assert mod.trace_batch() == "cpu"
+    mod.grow = mod.init_guide_strands = mod.connect_segments = lambda *a, **k: "cpu"
+    gpu.phg.install(mod, full=True)
+    try:
+        from paper_2604_05794_b200 import grow, link
+
+        assert mod.init_guide_strands is grow.init_guide_strands
+        assert mod.connect_segments is link.connect_segments
+        assert mod.grow is link.grow
+    finally:
+        gpu.phg.uninstall(mod)
+    assert mod.grow() == "cpu" and mod._make_pool() == "pool"
 
 
 def test_device_api_matches_host_api(gpu):
