@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--cpu-sample", type=int, default=0, help="seeds in the CPU sample")
     ap.add_argument("--sweep", action="store_true", help="time every trace-kernel variant")
     ap.add_argument("--no-driver", action="store_true", help="skip the batch-driver leg")
+    ap.add_argument("--e2e-chunk", type=int, default=0,
+                    help="seeds per chunk of the pipelined host path (0: library default)")
     return ap.parse_args()
 
 
@@ -443,7 +445,7 @@ def e2e_leg(args, tracer, field, params, s_host, d_host, per_rank, ws, dev, step
         # phg_trace_to_host: chunked, the D2H of chunk k overlaps the trace of chunk k+1
         return tracer.trace_to_host(field, params, pin_s.data_ptr(), pin_d.data_ptr(), n,
                                     out_off.data_ptr(), out_ent.data_ptr(), out_v.data_ptr(),
-                                    int(out_v.shape[0]), 0, stream.cuda_stream)
+                                    int(out_v.shape[0]), args.e2e_chunk, stream.cuda_stream)
 
     for _ in range(max(1, args.warmup - 1)):
         one()
@@ -459,7 +461,21 @@ def e2e_leg(args, tracer, field, params, s_host, d_host, per_rank, ws, dev, step
     if ws > 1:
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
     dt = float(tt.item())
+    # the PCIe floor of this leg: a plain pinned D2H of the same payload size
+    probe = torch.empty(min(total * 24, 2 << 30), dtype=torch.uint8, device=dev)
+    host = torch.empty(probe.numel(), dtype=torch.uint8).pin_memory()
+    host.copy_(probe, non_blocking=True)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(3):
+        host.copy_(probe, non_blocking=True)
+    torch.cuda.synchronize()
+    d2h_gbs = 3 * probe.numel() / (time.perf_counter() - t0) / 1e9
+    del probe, host
+    floor_ms = (total * 24 + (n + 1) * 8 + n) / d2h_gbs / 1e6
     return {"value": steps_per_trace * ws / dt, "unit": "steps/s",
+            "pcie_d2h_gbs": d2h_gbs, "pcie_floor_ms": floor_ms,
+            "frac_of_pcie_floor": floor_ms / (dt * 1e3), "chunk": args.e2e_chunk,
             "h2d_bytes_per_step": int(2 * n * 24), "d2h_bytes_per_step": int((n + 1) * 8 + n +
                                                                              total * 24),
             "ms_per_step": dt * 1e3,
