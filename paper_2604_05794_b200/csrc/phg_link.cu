@@ -439,6 +439,7 @@ phg_status phg_link(phg_ctx* c, const int64_t* offsets, const double* verts,
         d_root = c->g_out_rooted.as<uint8_t>();
         d_src = nullptr;  // traced if rooted else field
     }
+    if (n >= (1ll << 31)) return fail(PHG_ERR_INVALID, "phg_link: more than 2^31 segments");
     std::vector<long long> h_off;
     PHG_TRY(d2h(h_off, d_off, (size_t)n + 1, st));
     std::vector<uint8_t> h_root, h_src;
@@ -510,6 +511,8 @@ phg_status phg_link(phg_ctx* c, const int64_t* offsets, const double* verts,
         PHG_TRY(scan_lengths(c, cnt, n, poff, st));
         PHG_CUDA(cudaMemcpyAsync(&P, poff + n, 8, cudaMemcpyDeviceToHost, st));
         PHG_CUDA(cudaStreamSynchronize(st));
+        if (P >= (1ll << 31))
+            return fail(PHG_ERR_INVALID, "phg_link: %lld candidate pairs exceed 2^31", P);
         if (P > 0) {
             PHG_TRY(c->l_pd.ensure((size_t)P * 8));
             PHG_TRY(c->l_pij.ensure((size_t)P * 8 * 4));
