@@ -129,6 +129,30 @@ phg_status phg_grow_init(phg_ctx* c, phg_field* f, const phg_params_v1* p,
                          const phg_grow_params_v1* g, const double* seeds, const double* normals,
                          int64_t n, uint16_t* counts, int64_t* n_segments, int64_t* n_verts,
                          int64_t report[4], void* stream);
+/* The same driver as batch-level steps, for callers that interleave their own work between
+ * deferred-commit batches (the multi-GPU driver exchanges commits between ranks):
+ *   phg_grow_begin         load vol.counts, reset the session
+ *   phg_grow_scalp_batch   one batch of scalp seeds (phg.py:229-251) -> out = {segments
+ *                          added, commit ids exported}; export_commits=0 commits directly
+ *   phg_grow_field_begin   select the field seeds from the current counts (phg.py:266-275)
+ *   phg_grow_field_batch   field seeds [first, first+nb): +d / -d traces, join, keep, commit
+ *   phg_grow_commits       copy the last batch's exported commit ids (one per segment and
+ *                          distinct voxel; u32 linear voxel index)
+ *   phg_grow_apply         counts[id] += 1 for each id (the union of all ranks' exports)
+ *   phg_grow_end           write vol.counts back, finish the segment set (-> phg_grow_fetch,
+ *                          phg_link with offsets == NULL) */
+phg_status phg_grow_begin(phg_ctx* c, phg_field* f, const phg_params_v1* p,
+                          const phg_grow_params_v1* g, const uint16_t* counts, void* stream);
+phg_status phg_grow_scalp_batch(phg_ctx* c, const double* seeds, const double* normals,
+                                int64_t nb, int32_t export_commits, int64_t out[2], void* stream);
+phg_status phg_grow_field_begin(phg_ctx* c, int64_t* n_field_seeds, void* stream);
+phg_status phg_grow_field_batch(phg_ctx* c, int64_t first, int64_t nb, int32_t export_commits,
+                                int64_t out[2], void* stream);
+phg_status phg_grow_commits(phg_ctx* c, uint32_t* ids, void* stream);
+phg_status phg_grow_apply(phg_ctx* c, const uint32_t* ids, int64_t n, void* stream);
+phg_status phg_grow_end(phg_ctx* c, uint16_t* counts, int64_t* n_segments, int64_t* n_verts,
+                        int64_t report[4], void* stream);
+
 /* Segments of the last phg_grow_init in order (scalp segments in seed order, then field
  * segments): offsets (n_segments+1) i64, verts (n_verts,3) f64, rooted (n_segments) u8
  * (1 = Strand(rooted=True, source="traced"), 0 = Strand(rooted=False, source="field")).

@@ -27,6 +27,8 @@ EXPORTS = (
     "phg_last_steps", "phg_sample", "phg_last_error", "phg_abi_version", "phg_last_kernel_ms",
     "phg_last_variant", "phg_num_variants", "phg_selftest", "phg_grow_init", "phg_grow_fetch",
     "phg_trace_to_host", "phg_stnd_encode", "phg_field_from_oovl", "phg_link", "phg_link_fetch",
+    "phg_grow_begin", "phg_grow_scalp_batch", "phg_grow_field_begin", "phg_grow_field_batch",
+    "phg_grow_commits", "phg_grow_apply", "phg_grow_end",
 )
 
 
@@ -90,6 +92,14 @@ def _declare(lib):
                               ctypes.POINTER(I64), ctypes.POINTER(I64), ctypes.POINTER(I64), VP]),
         "phg_grow_fetch": (S, [VP, VP, VP, VP, VP]),
         "phg_stnd_encode": (S, [VP, VP, I64, VP, VP]),
+        "phg_grow_begin": (S, [VP, VP, ctypes.POINTER(Params), VP, VP, VP]),
+        "phg_grow_scalp_batch": (S, [VP, VP, VP, I64, ctypes.c_int32, ctypes.POINTER(I64), VP]),
+        "phg_grow_field_begin": (S, [VP, ctypes.POINTER(I64), VP]),
+        "phg_grow_field_batch": (S, [VP, I64, I64, ctypes.c_int32, ctypes.POINTER(I64), VP]),
+        "phg_grow_commits": (S, [VP, VP, VP]),
+        "phg_grow_apply": (S, [VP, VP, I64, VP]),
+        "phg_grow_end": (S, [VP, VP, ctypes.POINTER(I64), ctypes.POINTER(I64),
+                             ctypes.POINTER(I64), VP]),
         "phg_link": (S, [VP, VP, VP, VP, VP, I64, VP, I64, ctypes.POINTER(LinkParams),
                          ctypes.POINTER(I64), VP]),
         "phg_link_fetch": (S, [VP, VP, VP, VP, VP, VP, VP, VP]),

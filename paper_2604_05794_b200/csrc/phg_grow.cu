@@ -97,12 +97,32 @@ __device__ __forceinline__ bool set_insert(unsigned long long* T, int bits, uint
     }
 }
 
-// Add the vertices of one slab row to the warp's set, counting newly seen in-bounds voxels.
+// counts[lin] += 1, keeping the at_cap plane (counts >= cap, phg.py:236) current
+// incrementally: without uint16 wrap-around counts only grow, so a voxel turns "at cap" exactly
+// when its count reaches cap; a wrap raises `wrapped`, which forces a full rebuild
+__device__ __forceinline__ void bump_count(uint32_t* __restrict__ counts,
+                                           uint32_t* __restrict__ cap_bits, uint32_t cap,
+                                           unsigned int* __restrict__ wrapped, uint32_t lin) {
+    const uint32_t now = (atomicAdd(counts + lin, 1u) + 1u) & 0xffffu;
+    if (now == cap) atomicOr(cap_bits + (lin >> 5), 1u << (lin & 31));
+    if (now == 0u) atomicOr(wrapped, 1u);
+}
+
+// Where a segment's distinct voxels go: straight into counts (one rank), or appended to an
+// export list that every rank applies after an all-gather (multi-rank driver).
+struct CommitSink {
+    uint32_t* counts;
+    uint32_t* cap_bits;
+    uint32_t cap;
+    unsigned int* wrapped;
+    uint32_t* export_ids;                 // nullptr: commit directly
+    unsigned long long* export_cursor;
+};
+
+// Add the vertices of one slab row to the warp's set; commit newly seen in-bounds voxels.
 __device__ __forceinline__ void commit_row(const FieldView& F, const double* __restrict__ row,
                                            long long L, unsigned long long* T, int bits,
-                                           uint32_t epoch, uint32_t* __restrict__ counts,
-                                           uint32_t* __restrict__ cap_bits, uint32_t cap,
-                                           unsigned int* __restrict__ wrapped, int lane) {
+                                           uint32_t epoch, const CommitSink& K, int lane) {
     for (long long k = lane; k < L; k += 32) {
         // vol.voxel_of (volume.py:42-45) and in_bounds (:47-49)
         const int vx = floor_idx(grid_coord(F, row[3 * k + 0] - F.ox));
@@ -112,15 +132,22 @@ __device__ __forceinline__ void commit_row(const FieldView& F, const double* __r
             (unsigned)vz < (unsigned)F.nz) {
             const uint32_t lin = ((uint32_t)vx * F.ny + vy) * F.nz + vz;
             if (set_insert(T, bits, epoch, lin)) {
-                // keep the at_cap plane (counts >= cap, phg.py:236) current incrementally:
-                // without uint16 wrap-around counts only grow, so a voxel turns "at cap"
-                // exactly when its count reaches cap; a wrap forces a full rebuild
-                const uint32_t now = (atomicAdd(counts + lin, 1u) + 1u) & 0xffffu;
-                if (now == cap) atomicOr(cap_bits + (lin >> 5), 1u << (lin & 31));
-                if (now == 0u) atomicOr(wrapped, 1u);
+                if (K.export_ids)
+                    K.export_ids[atomicAdd(K.export_cursor, 1ull)] = lin;
+                else
+                    bump_count(K.counts, K.cap_bits, K.cap, K.wrapped, lin);
             }
         }
     }
+}
+
+// apply exported commits (all ranks' lists): counts[id] += 1 for each id
+__global__ void apply_commits_kernel(const uint32_t* __restrict__ ids, long long n,
+                                     uint32_t* __restrict__ counts, uint32_t* __restrict__ cap_bits,
+                                     uint32_t cap, unsigned int* __restrict__ wrapped) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        bump_count(counts, cap_bits, cap, wrapped, ids[i]);
 }
 
 // vol.counts[unique voxels of each valid segment] += 1 (phg.py:248-251, :299-302).  One warp per
@@ -132,9 +159,7 @@ __global__ void commit_kernel(FieldView F, const double* __restrict__ slab_a,
                               const double* __restrict__ slab_b,
                               const long long* __restrict__ keep_b,
                               const uint8_t* __restrict__ valid, long long n, size_t row_stride,
-                              uint32_t* __restrict__ counts, uint32_t* __restrict__ cap_bits,
-                              uint32_t cap, unsigned int* __restrict__ wrapped, int bits,
-                              unsigned long long* __restrict__ gtables) {
+                              CommitSink K, int bits, unsigned long long* __restrict__ gtables) {
     extern __shared__ unsigned long long smem_tables[];
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
@@ -148,10 +173,9 @@ __global__ void commit_kernel(FieldView F, const double* __restrict__ slab_a,
     for (long long i = gwarp; i < n; i += nwarps) {
         if (!valid[i]) continue;
         ++epoch;
-        commit_row(F, slab_a + (size_t)i * row_stride, keep_a[i], T, bits, epoch, counts,
-                   cap_bits, cap, wrapped, lane);
-        if (slab_b) commit_row(F, slab_b + (size_t)i * row_stride, keep_b[i], T, bits, epoch,
-                               counts, cap_bits, cap, wrapped, lane);
+        commit_row(F, slab_a + (size_t)i * row_stride, keep_a[i], T, bits, epoch, K, lane);
+        if (slab_b) commit_row(F, slab_b + (size_t)i * row_stride, keep_b[i], T, bits, epoch, K,
+                               lane);
         __syncwarp();
     }
 }
@@ -316,92 +340,129 @@ phg_status grow_keep(DevBuf& b, size_t used, size_t need, cudaStream_t st) {
     return PHG_OK;
 }
 
-struct GrowState {
-    phg_ctx* c;
-    phg_field* f;
-    const phg_params_v1* p;
-    const phg_grow_params_v1* g;
-    cudaStream_t st;
-    bool strict;
-    uint32_t* counts;    // device uint32 plane (vol.counts)
-    long long segs = 0;  // output segments so far
-    long long verts = 0; // output vertices so far
-    unsigned long long* misc = nullptr;  // [0] never_entered, [1] (u32) count wrapped
-    bool cap_valid = false;              // f->cap == (counts >= cap) for the current counts
+// ---- the batch-driver session ---------------------------------------------------------------
+// State of one init_guide_strands run, kept on the context between the batch-level entry points
+// (phg_grow_begin .. phg_grow_end); phg_grow_init composes them for the single-GPU case.
+struct GrowSession {
+    phg_field* f = nullptr;
+    phg_params_v1 p{};
+    phg_grow_params_v1 g{};
+    bool strict = false;
+    uint32_t* counts = nullptr;  // device uint32 plane (vol.counts), c->counts32
+    long long segs = 0, verts = 0, scalp_segs = 0, n_field = 0;
+    DevBuf misc;                 // [0] never-entered scalp seeds, [1] (u32) count wrapped
+    bool cap_valid = false;      // f->cap == (counts >= cap) for the current counts
+    DevBuf export_ids;           // commits of the last batch (multi-rank mode)
+    long long n_export = 0;
+    long long nf_seeds = 0;      // field seeds selected by phg_grow_field_begin
 };
 
-phg_status set_cap_plane(GrowState& S) {
+struct GrowCtx {  // per-call view
+    phg_ctx* c;
+    GrowSession* s;
+    cudaStream_t st;
+};
+
+phg_status set_cap_plane(GrowCtx& G) {
+    GrowSession& S = *G.s;
     if (S.strict) {
         S.f->has_cap = false;
         return PHG_OK;
     }
     S.f->has_cap = true;
-    if (S.cap_valid) return PHG_OK;  // maintained incrementally by the commit kernel
+    if (S.cap_valid) return PHG_OK;  // maintained incrementally by the commits
     const long long V = S.f->nvox();
     PHG_TRY(S.f->cap.ensure((size_t)((V + 31) / 32) * 4));
-    cap_from_counts_kernel<<<grid_for((V + 31) / 32 * 32, 256, num_sms() * 16), 256, 0, S.st>>>(
-        S.counts, V, (uint32_t)S.g->occupancy_cap, S.f->cap.as<uint32_t>());
+    cap_from_counts_kernel<<<grid_for((V + 31) / 32 * 32, 256, num_sms() * 16), 256, 0, G.st>>>(
+        S.counts, V, (uint32_t)S.g.occupancy_cap, S.f->cap.as<uint32_t>());
     PHG_CUDA(cudaGetLastError());
     S.cap_valid = true;
     return PHG_OK;
 }
 
-phg_status launch_commit(GrowState& S, const double* slab_a, const long long* keep_a,
+CommitSink direct_sink(GrowSession& S) {
+    return CommitSink{S.counts, S.f->cap.as<uint32_t>(), (uint32_t)S.g.occupancy_cap,
+                      (unsigned int*)(S.misc.as<unsigned long long>() + 1), nullptr, nullptr};
+}
+
+phg_status launch_commit(GrowCtx& G, const double* slab_a, const long long* keep_a,
                          const double* slab_b, const long long* keep_b, const uint8_t* valid,
-                         long long n) {
+                         long long n, CommitSink K) {
+    GrowSession& S = *G.s;
     const FieldView F = S.f->view();
-    const size_t rs = row_stride_doubles(S.p->max_vertices);
-    const long long max_entries = (long long)S.p->max_vertices * (slab_b ? 2 : 1);
+    const size_t rs = row_stride_doubles(S.p.max_vertices);
+    const long long max_entries = (long long)S.p.max_vertices * (slab_b ? 2 : 1);
     int bits = 6;
     while ((1ll << bits) < 2 * max_entries) ++bits;
     const size_t table_bytes = (size_t)8 << bits;
     const int warps_total = num_sms() * 16;
+    const int blocks = std::max(1, std::min(warps_total / kCommitWarps,
+                                            (int)((n + kCommitWarps - 1) / kCommitWarps)));
     if (table_bytes * kCommitWarps <= 200 * 1024) {
         const size_t smem = table_bytes * kCommitWarps;
         PHG_CUDA(cudaFuncSetAttribute(commit_kernel<false>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        const int blocks = std::max(1, std::min(warps_total / kCommitWarps,
-                                                (int)((n + kCommitWarps - 1) / kCommitWarps)));
-        commit_kernel<false><<<blocks, 32 * kCommitWarps, smem, S.st>>>(
-            F, slab_a, keep_a, slab_b, keep_b, valid, n, rs, S.counts, S.f->cap.as<uint32_t>(),
-            (uint32_t)S.g->occupancy_cap, (unsigned int*)(S.misc + 1), bits, nullptr);
+        commit_kernel<false><<<blocks, 32 * kCommitWarps, smem, G.st>>>(
+            F, slab_a, keep_a, slab_b, keep_b, valid, n, rs, K, bits, nullptr);
     } else {
-        const int blocks = std::max(1, std::min(warps_total / kCommitWarps,
-                                                (int)((n + kCommitWarps - 1) / kCommitWarps)));
-        PHG_TRY(S.c->g_hash.ensure(table_bytes * (size_t)blocks * kCommitWarps));
-        commit_kernel<true><<<blocks, 32 * kCommitWarps, 0, S.st>>>(
-            F, slab_a, keep_a, slab_b, keep_b, valid, n, rs, S.counts, S.f->cap.as<uint32_t>(),
-            (uint32_t)S.g->occupancy_cap, (unsigned int*)(S.misc + 1), bits,
-            S.c->g_hash.as<unsigned long long>());
+        PHG_TRY(G.c->g_hash.ensure(table_bytes * (size_t)blocks * kCommitWarps));
+        commit_kernel<true><<<blocks, 32 * kCommitWarps, 0, G.st>>>(
+            F, slab_a, keep_a, slab_b, keep_b, valid, n, rs, K, bits,
+            G.c->g_hash.as<unsigned long long>());
     }
     PHG_CUDA(cudaGetLastError());
     return PHG_OK;
 }
 
+// commit a batch: directly, or (export) into S.export_ids for an all-gather by the caller
+phg_status commit_batch(GrowCtx& G, const double* slab_a, const long long* keep_a,
+                        const double* slab_b, const long long* keep_b, const uint8_t* valid,
+                        long long n, long long max_ids, bool export_commits) {
+    GrowSession& S = *G.s;
+    S.n_export = 0;
+    if (S.strict) return PHG_OK;  // strict mode commits inside the trace
+    if (!export_commits) return launch_commit(G, slab_a, keep_a, slab_b, keep_b, valid, n,
+                                              direct_sink(S));
+    PHG_TRY(S.export_ids.ensure((size_t)std::max<long long>(max_ids, 1) * 4));
+    unsigned long long* cursor = S.misc.as<unsigned long long>() + 2;
+    PHG_CUDA(cudaMemsetAsync(cursor, 0, 8, G.st));
+    CommitSink K = direct_sink(S);
+    K.export_ids = S.export_ids.as<uint32_t>();
+    K.export_cursor = cursor;
+    PHG_TRY(launch_commit(G, slab_a, keep_a, slab_b, keep_b, valid, n, K));
+    PHG_CUDA(cudaMemcpyAsync(G.c->host_total + 3, cursor, 8, cudaMemcpyDeviceToHost, G.st));
+    PHG_CUDA(cudaStreamSynchronize(G.st));
+    S.n_export = G.c->host_total[3];
+    return PHG_OK;
+}
+
 // scans of lens / segment flags -> per-strand output offsets; returns batch totals (syncs)
-phg_status batch_offsets(GrowState& S, long long n, long long* lens, long long* segf,
+phg_status batch_offsets(GrowCtx& G, long long n, long long* lens, long long* segf,
                          long long* voff, long long* sidx, long long* nv, long long* ns) {
-    PHG_TRY(scan_lengths(S.c, lens, n, voff, S.st));
-    PHG_TRY(scan_lengths(S.c, segf, n, sidx, S.st));
-    PHG_CUDA(cudaMemcpyAsync(S.c->host_total, voff + n, 8, cudaMemcpyDeviceToHost, S.st));
-    PHG_CUDA(cudaMemcpyAsync(S.c->host_total + 1, sidx + n, 8, cudaMemcpyDeviceToHost, S.st));
-    PHG_CUDA(cudaMemcpyAsync(S.c->host_total + 2, S.misc + 1, 8, cudaMemcpyDeviceToHost, S.st));
-    PHG_CUDA(cudaStreamSynchronize(S.st));
-    *nv = S.c->host_total[0];
-    *ns = S.c->host_total[1];
-    if (S.c->host_total[2]) {  // a count wrapped past 65535: rebuild the cap plane exactly
+    GrowSession& S = *G.s;
+    PHG_TRY(scan_lengths(G.c, lens, n, voff, G.st));
+    PHG_TRY(scan_lengths(G.c, segf, n, sidx, G.st));
+    PHG_CUDA(cudaMemcpyAsync(G.c->host_total, voff + n, 8, cudaMemcpyDeviceToHost, G.st));
+    PHG_CUDA(cudaMemcpyAsync(G.c->host_total + 1, sidx + n, 8, cudaMemcpyDeviceToHost, G.st));
+    PHG_CUDA(cudaMemcpyAsync(G.c->host_total + 2, S.misc.as<unsigned long long>() + 1, 8,
+                             cudaMemcpyDeviceToHost, G.st));
+    PHG_CUDA(cudaStreamSynchronize(G.st));
+    *nv = G.c->host_total[0];
+    *ns = G.c->host_total[1];
+    if (G.c->host_total[2]) {  // a count wrapped past 65535: rebuild the cap plane exactly
         S.cap_valid = false;
-        PHG_CUDA(cudaMemsetAsync(S.misc + 1, 0, 8, S.st));
+        PHG_CUDA(cudaMemsetAsync(S.misc.as<unsigned long long>() + 1, 0, 8, G.st));
     }
     return PHG_OK;
 }
 
-phg_status ensure_output(GrowState& S, long long add_segs, long long add_verts) {
-    PHG_TRY(grow_keep(S.c->g_out_off, (size_t)S.segs * 8, (size_t)(S.segs + add_segs + 1) * 8,
-                      S.st));
-    PHG_TRY(grow_keep(S.c->g_out_rooted, (size_t)S.segs, (size_t)(S.segs + add_segs + 1), S.st));
-    PHG_TRY(grow_keep(S.c->g_out_verts, (size_t)S.verts * 24,
-                      (size_t)(S.verts + add_verts + 1) * 24, S.st));
+phg_status ensure_output(GrowCtx& G, long long add_segs, long long add_verts) {
+    GrowSession& S = *G.s;
+    PHG_TRY(grow_keep(G.c->g_out_off, (size_t)S.segs * 8, (size_t)(S.segs + add_segs + 1) * 8,
+                      G.st));
+    PHG_TRY(grow_keep(G.c->g_out_rooted, (size_t)S.segs, (size_t)(S.segs + add_segs + 1), G.st));
+    PHG_TRY(grow_keep(G.c->g_out_verts, (size_t)S.verts * 24,
+                      (size_t)(S.verts + add_verts + 1) * 24, G.st));
     return PHG_OK;
 }
 
@@ -411,9 +472,9 @@ struct BatchScratch {
     uint8_t* valid;
 };
 
-phg_status batch_scratch(GrowState& S, long long n, BatchScratch& B) {
-    PHG_TRY(S.c->g_misc.ensure((size_t)(n + 1) * 8 * 4 + (size_t)n + 64));
-    char* base = (char*)S.c->g_misc.p;
+phg_status batch_scratch(GrowCtx& G, long long n, BatchScratch& B) {
+    PHG_TRY(G.c->g_misc.ensure((size_t)(n + 1) * 8 * 4 + (size_t)n + 64));
+    char* base = (char*)G.c->g_misc.p;
     B.lens = (long long*)base;
     B.segf = B.lens + (n + 1);
     B.voff = B.segf + (n + 1);
@@ -422,144 +483,321 @@ phg_status batch_scratch(GrowState& S, long long n, BatchScratch& B) {
     return PHG_OK;
 }
 
-phg_status scalp_pass(GrowState& S, const double* d_pos, const double* d_dir, long long n) {
-    const long long bs = S.g->batch_size;
-    for (long long b0 = 0; b0 < n; b0 += bs) {
-        const long long nb = std::min(bs, n - b0);
-        PHG_TRY(set_cap_plane(S));
-        PHG_TRY(trace_core(S.c, S.f, S.p, d_pos + 3 * b0, d_dir + 3 * b0, nb,
-                           S.strict ? S.counts : nullptr, S.st));
-        BatchScratch B;
-        PHG_TRY(batch_scratch(S, nb, B));
-        const long long* keep = S.c->keep.as<long long>();
-        segment_select_kernel<<<grid_for(nb, 256), 256, 0, S.st>>>(
-            keep, S.c->entered.as<uint8_t>(), nb, B.lens, B.segf, B.valid, S.misc);
-        PHG_CUDA(cudaGetLastError());
-        if (!S.strict)
-            PHG_TRY(launch_commit(S, S.c->slab.as<double>(), keep, nullptr, nullptr, B.valid, nb));
-        long long nv = 0, ns = 0;
-        PHG_TRY(batch_offsets(S, nb, B.lens, B.segf, B.voff, B.sidx, &nv, &ns));
-        PHG_TRY(ensure_output(S, ns, nv));
-        gather_scalp_kernel<<<grid_for(nb * 32, 256, num_sms() * 16), 256, 0, S.st>>>(
-            S.c->slab.as<double>(), row_stride_doubles(S.p->max_vertices), keep, B.valid, B.voff,
-            B.sidx, nb, S.verts, S.segs, S.c->g_out_off.as<long long>(),
-            S.c->g_out_verts.as<double>(), S.c->g_out_rooted.as<uint8_t>());
-        PHG_CUDA(cudaGetLastError());
-        S.segs += ns;
-        S.verts += nv;
-    }
+// one deferred-commit batch of scalp seeds (phg.py:229-251)
+phg_status scalp_batch(GrowCtx& G, const double* d_pos, const double* d_dir, long long nb,
+                       bool export_commits, long long* segs_added) {
+    GrowSession& S = *G.s;
+    phg_ctx* c = G.c;
+    *segs_added = 0;
+    S.n_export = 0;
+    if (nb == 0) return PHG_OK;
+    PHG_TRY(set_cap_plane(G));
+    PHG_TRY(trace_core(c, S.f, &S.p, d_pos, d_dir, nb, S.strict ? S.counts : nullptr, G.st));
+    BatchScratch B;
+    PHG_TRY(batch_scratch(G, nb, B));
+    const long long* keep = c->keep.as<long long>();
+    segment_select_kernel<<<grid_for(nb, 256), 256, 0, G.st>>>(
+        keep, c->entered.as<uint8_t>(), nb, B.lens, B.segf, B.valid, S.misc.as<unsigned long long>());
+    PHG_CUDA(cudaGetLastError());
+    // direct commits go before the synchronising offsets step, which also picks up a uint16
+    // wrap flag they may raise; exported commits need the batch size to size their list
+    if (!export_commits)
+        PHG_TRY(commit_batch(G, c->slab.as<double>(), keep, nullptr, nullptr, B.valid, nb, 0,
+                             false));
+    long long nv = 0, ns = 0;
+    PHG_TRY(batch_offsets(G, nb, B.lens, B.segf, B.voff, B.sidx, &nv, &ns));
+    if (export_commits)
+        PHG_TRY(commit_batch(G, c->slab.as<double>(), keep, nullptr, nullptr, B.valid, nb, nv,
+                             true));
+    PHG_TRY(ensure_output(G, ns, nv));
+    gather_scalp_kernel<<<grid_for(nb * 32, 256, num_sms() * 16), 256, 0, G.st>>>(
+        c->slab.as<double>(), row_stride_doubles(S.p.max_vertices), keep, B.valid, B.voff, B.sidx,
+        nb, S.verts, S.segs, c->g_out_off.as<long long>(), c->g_out_verts.as<double>(),
+        c->g_out_rooted.as<uint8_t>());
+    PHG_CUDA(cudaGetLastError());
+    S.segs += ns;
+    S.verts += nv;
+    S.scalp_segs = S.segs;
+    *segs_added = ns;
     return PHG_OK;
 }
 
-phg_status field_pass(GrowState& S, long long* n_field_seeds) {
-    *n_field_seeds = 0;
-    phg_ctx* c = S.c;
+// field seeds (phg.py:266-275): unvisited occupied voxels, strided, centres + unit ori
+phg_status field_begin(GrowCtx& G) {
+    GrowSession& S = *G.s;
+    phg_ctx* c = G.c;
+    S.nf_seeds = 0;
+    S.n_field = 0;
     const long long V = S.f->nvox();
     const FieldView F = S.f->view();
     long long* d_count = (long long*)c->counters.p + 4;
     thrust::counting_iterator<uint32_t> iota(0);
-    // 1. unvisited occupied voxels, ascending linear index == np.argwhere's C order
     PHG_TRY(c->g_flags.ensure((size_t)V));
     PHG_TRY(c->g_sel.ensure((size_t)V * 4));
     uint8_t* flags = c->g_flags.as<uint8_t>();
     uint32_t* unvisited = c->g_sel.as<uint32_t>();
-    unvisited_flag_kernel<<<grid_for(V, 256, num_sms() * 16), 256, 0, S.st>>>(F.vox, S.counts, V,
+    unvisited_flag_kernel<<<grid_for(V, 256, num_sms() * 16), 256, 0, G.st>>>(F.vox, S.counts, V,
                                                                               flags);
     PHG_CUDA(cudaGetLastError());
     size_t tmp = 0;
-    cub::DeviceSelect::Flagged(nullptr, tmp, iota, flags, unvisited, d_count, V, S.st);
+    cub::DeviceSelect::Flagged(nullptr, tmp, iota, flags, unvisited, d_count, V, G.st);
     PHG_TRY(c->cub_tmp.ensure(tmp));
     PHG_CUDA(cub::DeviceSelect::Flagged(c->cub_tmp.p, tmp, iota, flags, unvisited, d_count, V,
-                                        S.st));
-    PHG_CUDA(cudaMemcpyAsync(c->host_total, d_count, 8, cudaMemcpyDeviceToHost, S.st));
-    PHG_CUDA(cudaStreamSynchronize(S.st));
+                                        G.st));
+    PHG_CUDA(cudaMemcpyAsync(c->host_total, d_count, 8, cudaMemcpyDeviceToHost, G.st));
+    PHG_CUDA(cudaStreamSynchronize(G.st));
     const long long U = c->host_total[0];
-    if (U == 0) return PHG_OK;
-    // 2. stride down to field_seeds voxels
+    if (U == 0 || S.g.field_seeds <= 0) return PHG_OK;
     long long m = U;
     const uint32_t* picked = unvisited;
-    if (U > S.g->field_seeds) {
-        m = S.g->field_seeds;
+    if (U > S.g.field_seeds) {
+        m = S.g.field_seeds;
         PHG_TRY(c->g_pick.ensure((size_t)m * 4));
-        stride_pick_kernel<<<grid_for(m, 256), 256, 0, S.st>>>(unvisited, U, m,
+        stride_pick_kernel<<<grid_for(m, 256), 256, 0, G.st>>>(unvisited, U, m,
                                                                 c->g_pick.as<uint32_t>());
         PHG_CUDA(cudaGetLastError());
         picked = c->g_pick.as<uint32_t>();
     }
-    // 3. centres + unit orientation, then drop rows with |ori| <= 1e-9
     PHG_TRY(c->g_raw.ensure((size_t)m * 48 + (size_t)m));
     double* raw_pos = c->g_raw.as<double>();
     double* raw_dir = raw_pos + 3 * m;
     uint8_t* keepf = (uint8_t*)(raw_dir + 3 * m);
-    field_seed_kernel<<<grid_for(m, 256), 256, 0, S.st>>>(F, picked, m, raw_pos, raw_dir, keepf);
+    field_seed_kernel<<<grid_for(m, 256), 256, 0, G.st>>>(F, picked, m, raw_pos, raw_dir, keepf);
     PHG_CUDA(cudaGetLastError());
     PHG_TRY(c->g_rows.ensure((size_t)m * 4));
     uint32_t* rows = c->g_rows.as<uint32_t>();
     tmp = 0;
-    cub::DeviceSelect::Flagged(nullptr, tmp, iota, keepf, rows, d_count, m, S.st);
+    cub::DeviceSelect::Flagged(nullptr, tmp, iota, keepf, rows, d_count, m, G.st);
     PHG_TRY(c->cub_tmp.ensure(tmp));
-    PHG_CUDA(cub::DeviceSelect::Flagged(c->cub_tmp.p, tmp, iota, keepf, rows, d_count, m, S.st));
-    PHG_CUDA(cudaMemcpyAsync(c->host_total, d_count, 8, cudaMemcpyDeviceToHost, S.st));
-    PHG_CUDA(cudaStreamSynchronize(S.st));
+    PHG_CUDA(cub::DeviceSelect::Flagged(c->cub_tmp.p, tmp, iota, keepf, rows, d_count, m, G.st));
+    PHG_CUDA(cudaMemcpyAsync(c->host_total, d_count, 8, cudaMemcpyDeviceToHost, G.st));
+    PHG_CUDA(cudaStreamSynchronize(G.st));
     const long long nf = c->host_total[0];
-    *n_field_seeds = nf;
+    S.nf_seeds = nf;
+    S.n_field = nf;
     if (nf == 0) return PHG_OK;
     PHG_TRY(c->g_fpos.ensure((size_t)nf * 24));
     PHG_TRY(c->g_fdir.ensure((size_t)nf * 24));
-    double* pos = c->g_fpos.as<double>();
-    double* dir = c->g_fdir.as<double>();
-    row_gather_kernel<<<grid_for(nf, 256), 256, 0, S.st>>>(raw_pos, raw_dir, rows, nf, pos, dir);
+    row_gather_kernel<<<grid_for(nf, 256), 256, 0, G.st>>>(raw_pos, raw_dir, rows, nf,
+                                                           c->g_fpos.as<double>(),
+                                                           c->g_fdir.as<double>());
     PHG_CUDA(cudaGetLastError());
-    // 4. batches: trace +d and -d against the same frozen plane, join, keep, commit
-    const long long bs = S.g->batch_size;
-    const size_t rs = row_stride_doubles(S.p->max_vertices);
-    for (long long b0 = 0; b0 < nf; b0 += bs) {
-        const long long nb = std::min(bs, nf - b0);
-        PHG_TRY(set_cap_plane(S));
-        PHG_TRY(trace_core(S.c, S.f, S.p, pos + 3 * b0, dir + 3 * b0, nb,
-                           S.strict ? S.counts : nullptr, S.st));
-        // keep the forward trace aside
-        swap_buf(S.c->slab, S.c->g_slab2);
-        swap_buf(S.c->keep, S.c->g_keep2);
-        swap_buf(S.c->entered, S.c->g_ent2);
-        PHG_TRY(S.c->g_neg_dir.ensure((size_t)nb * 24));
-        double* ndir = S.c->g_neg_dir.as<double>();
-        negate_kernel<<<grid_for(nb * 3, 256, num_sms() * 16), 256, 0, S.st>>>(dir + 3 * b0, ndir,
-                                                                                nb * 3);
-        PHG_CUDA(cudaGetLastError());
-        if (!S.strict) PHG_TRY(set_cap_plane(S));  // identical plane: no commits in between
-        PHG_TRY(trace_core(S.c, S.f, S.p, pos + 3 * b0, ndir, nb, S.strict ? S.counts : nullptr,
-                           S.st));
-        const double* slab_f = S.c->g_slab2.as<double>();
-        const long long* keep_f = S.c->g_keep2.as<long long>();
-        const uint8_t* ent_f = S.c->g_ent2.as<uint8_t>();
-        const double* slab_b = S.c->slab.as<double>();
-        const long long* keep_b = S.c->keep.as<long long>();
-        const uint8_t* ent_b = S.c->entered.as<uint8_t>();
-        BatchScratch B;
-        PHG_TRY(batch_scratch(S, nb, B));
-        join_select_kernel<<<grid_for(nb, 256), 256, 0, S.st>>>(keep_f, ent_f, keep_b, ent_b, nb,
-                                                                B.lens, B.segf, B.valid);
-        PHG_CUDA(cudaGetLastError());
-        if (!S.strict) PHG_TRY(launch_commit(S, slab_f, keep_f, slab_b, keep_b, B.valid, nb));
-        long long nv = 0, ns = 0;
-        PHG_TRY(batch_offsets(S, nb, B.lens, B.segf, B.voff, B.sidx, &nv, &ns));
-        PHG_TRY(ensure_output(S, ns, nv));
-        gather_joined_kernel<<<grid_for(nb * 32, 256, num_sms() * 16), 256, 0, S.st>>>(
-            slab_f, slab_b, rs, keep_f, keep_b, B.valid, B.voff, B.sidx, nb, S.verts, S.segs,
-            S.c->g_out_off.as<long long>(), S.c->g_out_verts.as<double>(),
-            S.c->g_out_rooted.as<uint8_t>());
-        PHG_CUDA(cudaGetLastError());
-        S.segs += ns;
-        S.verts += nv;
+    return PHG_OK;
+}
+
+// one batch of field seeds [first, first + nb): trace +d and -d against the same frozen plane,
+// join, keep, commit (phg.py:277-302)
+phg_status field_batch(GrowCtx& G, long long first, long long nb, bool export_commits,
+                       long long* segs_added) {
+    GrowSession& S = *G.s;
+    phg_ctx* c = G.c;
+    *segs_added = 0;
+    S.n_export = 0;
+    if (nb == 0) return PHG_OK;
+    const double* pos = c->g_fpos.as<double>() + 3 * first;
+    const double* dir = c->g_fdir.as<double>() + 3 * first;
+    const size_t rs = row_stride_doubles(S.p.max_vertices);
+    PHG_TRY(set_cap_plane(G));
+    PHG_TRY(trace_core(c, S.f, &S.p, pos, dir, nb, S.strict ? S.counts : nullptr, G.st));
+    swap_buf(c->slab, c->g_slab2);  // keep the forward trace aside
+    swap_buf(c->keep, c->g_keep2);
+    swap_buf(c->entered, c->g_ent2);
+    PHG_TRY(c->g_neg_dir.ensure((size_t)nb * 24));
+    double* ndir = c->g_neg_dir.as<double>();
+    negate_kernel<<<grid_for(nb * 3, 256, num_sms() * 16), 256, 0, G.st>>>(dir, ndir, nb * 3);
+    PHG_CUDA(cudaGetLastError());
+    if (!S.strict) PHG_TRY(set_cap_plane(G));  // identical plane: no commits in between
+    PHG_TRY(trace_core(c, S.f, &S.p, pos, ndir, nb, S.strict ? S.counts : nullptr, G.st));
+    const double* slab_f = c->g_slab2.as<double>();
+    const long long* keep_f = c->g_keep2.as<long long>();
+    const uint8_t* ent_f = c->g_ent2.as<uint8_t>();
+    const double* slab_b = c->slab.as<double>();
+    const long long* keep_b = c->keep.as<long long>();
+    const uint8_t* ent_b = c->entered.as<uint8_t>();
+    BatchScratch B;
+    PHG_TRY(batch_scratch(G, nb, B));
+    join_select_kernel<<<grid_for(nb, 256), 256, 0, G.st>>>(keep_f, ent_f, keep_b, ent_b, nb,
+                                                            B.lens, B.segf, B.valid);
+    PHG_CUDA(cudaGetLastError());
+    if (!export_commits)
+        PHG_TRY(commit_batch(G, slab_f, keep_f, slab_b, keep_b, B.valid, nb, 0, false));
+    long long nv = 0, ns = 0;
+    PHG_TRY(batch_offsets(G, nb, B.lens, B.segf, B.voff, B.sidx, &nv, &ns));
+    // a joined segment's voxels are those of its two traces: at most L + 1 distinct ids
+    if (export_commits)
+        PHG_TRY(commit_batch(G, slab_f, keep_f, slab_b, keep_b, B.valid, nb, nv + ns, true));
+    PHG_TRY(ensure_output(G, ns, nv));
+    gather_joined_kernel<<<grid_for(nb * 32, 256, num_sms() * 16), 256, 0, G.st>>>(
+        slab_f, slab_b, rs, keep_f, keep_b, B.valid, B.voff, B.sidx, nb, S.verts, S.segs,
+        c->g_out_off.as<long long>(), c->g_out_verts.as<double>(), c->g_out_rooted.as<uint8_t>());
+    PHG_CUDA(cudaGetLastError());
+    S.segs += ns;
+    S.verts += nv;
+    *segs_added = ns;
+    return PHG_OK;
+}
+
+GrowSession* session(phg_ctx* c) { return static_cast<GrowSession*>(c->grow_session); }
+
+}  // namespace
+
+void grow_session_free(void* s) { delete static_cast<GrowSession*>(s); }
+
+}  // namespace phg
+
+extern "C" {
+
+phg_status phg_grow_begin(phg_ctx* c, phg_field* f, const phg_params_v1* p,
+                          const phg_grow_params_v1* g, const uint16_t* counts, void* stream) {
+    if (!c || !f || !p || !g || !counts) return fail(PHG_ERR_INVALID, "phg_grow_begin: null argument");
+    if (g->batch_size < 1 || g->occupancy_cap < 1)
+        return fail(PHG_ERR_INVALID, "phg_grow_begin: invalid batch_size / occupancy_cap");
+    if (p->max_vertices < 1)
+        return fail(PHG_ERR_INVALID, "phg_grow_begin: max_vertices must be >= 1");
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev != f->device)
+        return fail(PHG_ERR_INVALID, "phg_grow_begin: field lives on device %d", f->device);
+    cudaStream_t st = as_stream(stream);
+    c->grow_ready = false;
+    if (!c->grow_session) c->grow_session = new GrowSession();
+    GrowSession& S = *session(c);
+    S.f = f;
+    S.p = *p;
+    S.g = *g;
+    S.strict = (p->flags & PHG_FLAG_STRICT) != 0;
+    S.segs = S.verts = S.scalp_segs = S.n_field = S.n_export = S.nf_seeds = 0;
+    S.cap_valid = false;
+    const long long V = f->nvox();
+    PHG_TRY(c->counts32.ensure((size_t)V * 4));
+    S.counts = c->counts32.as<uint32_t>();
+    const void* d_counts = nullptr;
+    PHG_TRY(to_device(counts, (size_t)V * 2, c->live_stage, &d_counts, st));
+    u16_to_u32<<<grid_for(V, 256, num_sms() * 16), 256, 0, st>>>((const uint16_t*)d_counts,
+                                                                S.counts, V);
+    PHG_CUDA(cudaGetLastError());
+    PHG_TRY(c->counters.ensure(64));
+    PHG_CUDA(cudaMemsetAsync(c->counters.p, 0, 64, st));
+    PHG_TRY(S.misc.ensure(64));
+    PHG_CUDA(cudaMemsetAsync(S.misc.p, 0, 64, st));
+    PHG_CUDA(cudaStreamSynchronize(st));  // host counts may be released after return
+    return PHG_OK;
+}
+
+phg_status phg_grow_scalp_batch(phg_ctx* c, const double* seeds, const double* normals,
+                                int64_t nb, int32_t export_commits, int64_t out[2], void* stream) {
+    if (!c || !out || nb < 0 || (nb > 0 && (!seeds || !normals)))
+        return fail(PHG_ERR_INVALID, "phg_grow_scalp_batch: bad argument");
+    if (!session(c)) return fail(PHG_ERR_STATE, "phg_grow_scalp_batch: no phg_grow_begin");
+    cudaStream_t st = as_stream(stream);
+    GrowCtx G{c, session(c), st};
+    const void *d_pos = nullptr, *d_dir = nullptr;
+    PHG_TRY(to_device(seeds, (size_t)nb * 24, c->g_seeds_pos, &d_pos, st));
+    PHG_TRY(to_device(normals, (size_t)nb * 24, c->g_seeds_dir, &d_dir, st));
+    long long added = 0;
+    PHG_TRY(scalp_batch(G, (const double*)d_pos, (const double*)d_dir, nb, export_commits != 0,
+                        &added));
+    out[0] = added;
+    out[1] = G.s->n_export;
+    return PHG_OK;
+}
+
+phg_status phg_grow_field_begin(phg_ctx* c, int64_t* n_field_seeds, void* stream) {
+    if (!c || !n_field_seeds) return fail(PHG_ERR_INVALID, "phg_grow_field_begin: null argument");
+    if (!session(c)) return fail(PHG_ERR_STATE, "phg_grow_field_begin: no phg_grow_begin");
+    GrowCtx G{c, session(c), as_stream(stream)};
+    PHG_TRY(field_begin(G));
+    *n_field_seeds = G.s->nf_seeds;
+    return PHG_OK;
+}
+
+phg_status phg_grow_field_batch(phg_ctx* c, int64_t first, int64_t nb, int32_t export_commits,
+                                int64_t out[2], void* stream) {
+    if (!c || !out || first < 0 || nb < 0)
+        return fail(PHG_ERR_INVALID, "phg_grow_field_batch: bad argument");
+    if (!session(c)) return fail(PHG_ERR_STATE, "phg_grow_field_batch: no phg_grow_begin");
+    GrowCtx G{c, session(c), as_stream(stream)};
+    if (first + nb > G.s->nf_seeds)
+        return fail(PHG_ERR_INVALID, "phg_grow_field_batch: [%lld, %lld) beyond %lld field seeds",
+                    (long long)first, (long long)(first + nb), G.s->nf_seeds);
+    long long added = 0;
+    PHG_TRY(field_batch(G, first, nb, export_commits != 0, &added));
+    out[0] = added;
+    out[1] = G.s->n_export;
+    return PHG_OK;
+}
+
+phg_status phg_grow_commits(phg_ctx* c, uint32_t* ids, void* stream) {
+    if (!c || !session(c)) return fail(PHG_ERR_STATE, "phg_grow_commits: no session");
+    GrowSession& S = *session(c);
+    if (S.n_export && !ids) return fail(PHG_ERR_INVALID, "phg_grow_commits: null ids");
+    cudaStream_t st = as_stream(stream);
+    if (S.n_export)
+        PHG_CUDA(cudaMemcpyAsync(ids, S.export_ids.p, (size_t)S.n_export * 4, cudaMemcpyDefault, st));
+    PHG_CUDA(cudaStreamSynchronize(st));
+    return PHG_OK;
+}
+
+phg_status phg_grow_apply(phg_ctx* c, const uint32_t* ids, int64_t n, void* stream) {
+    if (!c || !session(c)) return fail(PHG_ERR_STATE, "phg_grow_apply: no session");
+    if (n < 0 || (n > 0 && !ids)) return fail(PHG_ERR_INVALID, "phg_grow_apply: bad ids");
+    GrowSession& S = *session(c);
+    if (S.strict || n == 0) return PHG_OK;
+    cudaStream_t st = as_stream(stream);
+    DevBuf stage;
+    const void* d_ids = nullptr;
+    PHG_TRY(to_device(ids, (size_t)n * 4, stage, &d_ids, st));
+    GrowCtx G{c, &S, st};
+    PHG_TRY(set_cap_plane(G));  // the plane must exist before incremental updates
+    const CommitSink K = direct_sink(S);
+    apply_commits_kernel<<<grid_for(n, 256, num_sms() * 16), 256, 0, st>>>(
+        (const uint32_t*)d_ids, n, K.counts, K.cap_bits, K.cap, K.wrapped);
+    PHG_CUDA(cudaGetLastError());
+    // a wrapped count invalidates the incremental plane
+    PHG_CUDA(cudaMemcpyAsync(c->host_total + 2, S.misc.as<unsigned long long>() + 1, 8,
+                             cudaMemcpyDeviceToHost, st));
+    PHG_CUDA(cudaStreamSynchronize(st));
+    if (c->host_total[2]) {
+        S.cap_valid = false;
+        PHG_CUDA(cudaMemsetAsync(S.misc.as<unsigned long long>() + 1, 0, 8, st));
     }
     return PHG_OK;
 }
 
-}  // namespace
-}  // namespace phg
-
-extern "C" {
+phg_status phg_grow_end(phg_ctx* c, uint16_t* counts, int64_t* n_segments, int64_t* n_verts,
+                        int64_t report[4], void* stream) {
+    if (!c || !session(c)) return fail(PHG_ERR_STATE, "phg_grow_end: no session");
+    if (!counts || !n_segments || !n_verts || !report)
+        return fail(PHG_ERR_INVALID, "phg_grow_end: null argument");
+    GrowSession& S = *session(c);
+    cudaStream_t st = as_stream(stream);
+    GrowCtx G{c, &S, st};
+    S.f->has_cap = false;  // the driver overwrote the field's cap plane; leave none behind
+    const long long V = S.f->nvox();
+    const bool counts_dev = is_device_ptr(counts);
+    PHG_TRY(c->live_stage.ensure((size_t)V * 2));
+    uint16_t* dst16 = counts_dev ? counts : c->live_stage.as<uint16_t>();
+    u32_to_u16<<<grid_for(V, 256, num_sms() * 16), 256, 0, st>>>(S.counts, dst16, V);
+    PHG_CUDA(cudaGetLastError());
+    if (!counts_dev)
+        PHG_CUDA(cudaMemcpyAsync(counts, dst16, (size_t)V * 2, cudaMemcpyDeviceToHost, st));
+    unsigned long long never = 0;
+    PHG_CUDA(cudaMemcpyAsync(&never, S.misc.p, 8, cudaMemcpyDeviceToHost, st));
+    PHG_TRY(ensure_output(G, 0, 0));
+    PHG_CUDA(cudaMemcpyAsync(c->g_out_off.as<long long>() + S.segs, &S.verts, 8,
+                             cudaMemcpyHostToDevice, st));
+    PHG_CUDA(cudaStreamSynchronize(st));
+    report[0] = (int64_t)never;
+    report[1] = S.scalp_segs;
+    report[2] = S.n_field;
+    report[3] = S.segs - S.scalp_segs;
+    *n_segments = S.segs;
+    *n_verts = S.verts;
+    c->grow_segs = S.segs;
+    c->grow_verts = S.verts;
+    c->grow_ready = true;
+    return PHG_OK;
+}
 
 phg_status phg_grow_init(phg_ctx* c, phg_field* f, const phg_params_v1* p,
                          const phg_grow_params_v1* g, const double* seeds, const double* normals,
@@ -568,35 +806,10 @@ phg_status phg_grow_init(phg_ctx* c, phg_field* f, const phg_params_v1* p,
     if (!c || !f || !p || !g || !counts || !n_segments || !n_verts || !report)
         return fail(PHG_ERR_INVALID, "phg_grow_init: null argument");
     if (n < 0) return fail(PHG_ERR_INVALID, "phg_grow_init: negative seed count");
-    if (n > 0 && (!seeds || !normals))
-        return fail(PHG_ERR_INVALID, "phg_grow_init: null seeds");
-    if (g->batch_size < 1 || g->occupancy_cap < 1)
-        return fail(PHG_ERR_INVALID, "phg_grow_init: invalid batch_size / occupancy_cap");
-    if (p->max_vertices < 1)
-        return fail(PHG_ERR_INVALID, "phg_grow_init: max_vertices must be >= 1");
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (dev != f->device)
-        return fail(PHG_ERR_INVALID, "phg_grow_init: field lives on device %d", f->device);
+    if (n > 0 && (!seeds || !normals)) return fail(PHG_ERR_INVALID, "phg_grow_init: null seeds");
     cudaStream_t st = as_stream(stream);
-    c->grow_ready = false;
-    GrowState S{c, f, p, g, st, (p->flags & PHG_FLAG_STRICT) != 0, nullptr};
-    const long long V = f->nvox();
-    PHG_TRY(c->counts32.ensure((size_t)V * 4));
-    S.counts = c->counts32.as<uint32_t>();
-    const bool counts_dev = is_device_ptr(counts);
-    const void* d_counts = nullptr;
-    PHG_TRY(to_device(counts, (size_t)V * 2, c->live_stage, &d_counts, st));
-    u16_to_u32<<<grid_for(V, 256, num_sms() * 16), 256, 0, st>>>((const uint16_t*)d_counts,
-                                                                S.counts, V);
-    PHG_CUDA(cudaGetLastError());
-    PHG_TRY(c->counters.ensure(64));
-    PHG_CUDA(cudaMemsetAsync(c->counters.p, 0, 64, st));
-    DevBuf misc_buf;  // [0] = never-entered scalp seeds
-    PHG_TRY(misc_buf.ensure(64));
-    PHG_CUDA(cudaMemsetAsync(misc_buf.p, 0, 64, st));
-    unsigned long long* misc = misc_buf.as<unsigned long long>();
-    S.misc = misc;
+    PHG_TRY(phg_grow_begin(c, f, p, g, counts, stream));
+    GrowCtx G{c, session(c), st};
     const void *d_pos = nullptr, *d_dir = nullptr;
     if (n > 0) {
         PHG_TRY(to_device(seeds, (size_t)n * 24, c->g_seeds_pos, &d_pos, st));
@@ -604,35 +817,23 @@ phg_status phg_grow_init(phg_ctx* c, phg_field* f, const phg_params_v1* p,
     }
     PHG_CUDA(cudaEventRecord(c->ev[0], st));  // device window: uploads done .. downloads begin
     phg_status s = PHG_OK;
-    if (n > 0) s = scalp_pass(S, (const double*)d_pos, (const double*)d_dir, n);
-    long long scalp_segs = S.segs;
-    long long n_field = 0;
-    if (s == PHG_OK && n > 0 && g->field_seeds > 0) s = field_pass(S, &n_field);
-    f->has_cap = false;  // the driver overwrote the field's cap plane; leave none behind
-    if (s != PHG_OK) return s;
+    const long long bs = g->batch_size;
+    long long added = 0;
+    for (long long b0 = 0; s == PHG_OK && b0 < n; b0 += bs)
+        s = scalp_batch(G, (const double*)d_pos + 3 * b0, (const double*)d_dir + 3 * b0,
+                        std::min(bs, n - b0), false, &added);
+    if (s == PHG_OK && n > 0 && g->field_seeds > 0) {
+        s = field_begin(G);
+        for (long long b0 = 0; s == PHG_OK && b0 < G.s->nf_seeds; b0 += bs)
+            s = field_batch(G, b0, std::min(bs, G.s->nf_seeds - b0), false, &added);
+    }
+    if (s != PHG_OK) {
+        f->has_cap = false;
+        return s;
+    }
     PHG_CUDA(cudaEventRecord(c->ev[2], st));
-    // counts back to vol.counts (uint16 wrap like np ndarray +=)
-    uint16_t* dst16 = counts_dev ? counts : c->live_stage.as<uint16_t>();
-    u32_to_u16<<<grid_for(V, 256, num_sms() * 16), 256, 0, st>>>(S.counts, dst16, V);
-    PHG_CUDA(cudaGetLastError());
-    if (!counts_dev)
-        PHG_CUDA(cudaMemcpyAsync(counts, dst16, (size_t)V * 2, cudaMemcpyDeviceToHost, st));
-    unsigned long long never = 0;
-    PHG_CUDA(cudaMemcpyAsync(&never, misc, 8, cudaMemcpyDeviceToHost, st));
-    PHG_TRY(ensure_output(S, 0, 0));
-    PHG_CUDA(cudaMemcpyAsync(c->g_out_off.as<long long>() + S.segs, &S.verts, 8,
-                             cudaMemcpyHostToDevice, st));
-    PHG_CUDA(cudaStreamSynchronize(st));
+    PHG_TRY(phg_grow_end(c, counts, n_segments, n_verts, report, stream));
     cudaEventElapsedTime(&c->last_total_ms, c->ev[0], c->ev[2]);
-    report[0] = (int64_t)never;
-    report[1] = scalp_segs;
-    report[2] = n_field;
-    report[3] = S.segs - scalp_segs;
-    *n_segments = S.segs;
-    *n_verts = S.verts;
-    c->grow_segs = S.segs;
-    c->grow_verts = S.verts;
-    c->grow_ready = true;
     return PHG_OK;
 }
 

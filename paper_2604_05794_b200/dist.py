@@ -76,6 +76,120 @@ def trace_sharded(trace_fn, seed_pos, seed_dir, group=None, device="cpu"):
     return off + info.vert_start, verts, ent, info
 
 
+def _allgather_v(t, group=None):
+    """All-gather of 1-D tensors of different lengths (pad to the longest)."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    n = torch.tensor([t.numel()], dtype=torch.int64, device=t.device)
+    ns = [torch.empty_like(n) for _ in range(world)]
+    dist.all_gather(ns, n, group=group)
+    sizes = [int(x.item()) for x in ns]
+    pad = torch.zeros(max(max(sizes), 1), dtype=t.dtype, device=t.device)
+    pad[: t.numel()] = t
+    outs = [torch.empty_like(pad) for _ in range(world)]
+    dist.all_gather(outs, pad, group=group)
+    return [o[:s] for o, s in zip(outs, sizes)]
+
+
+def init_guide_strands_multirank(seeds, normals, counts, params, backend, group=None,
+                                 device="cpu", force_export=False):
+    """init_guide_strands (phg.py:210-303) over all ranks of ``group``, exactly.
+
+    Every deferred-commit batch -- scalp batches of ``params.batch_size`` seeds, then the
+    field-seed batches -- is split in contiguous rank slices (phg.py:201's split); each rank
+    traces its slice against the SAME frozen cap plane (every rank holds an identical
+    ``counts`` replica), exports its commits (one voxel id per segment and distinct voxel,
+    phg.py:248-251), and all ranks apply the all-gathered union before the next batch.  This
+    is the one collective per batch the deferred-commit semantics require.
+    ``backend`` runs the batch steps: grow.DeviceGrowSession on a GPU (NCCL, CUDA ids) or an
+    oracle session on the CPU (gloo tests).  ``counts`` (uint16, vol.counts) is updated in
+    place on every rank.  ``device`` is where the collectives run ("cuda" for NCCL, "cpu"
+    for gloo); ``force_export`` exercises the export/all-gather/apply path on one rank.
+
+    Returns (offsets, verts, rooted, report) of the full segment set, in the reference's
+    order, on rank 0 and None on the other ranks.
+    """
+    import torch
+    import torch.distributed as dist
+
+    if bool(params.strict):
+        from .errors import ConfigError
+
+        raise ConfigError("strict mode commits after every step of every strand; run it on one rank")
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    export = world > 1 or force_export
+    bs = int(params.batch_size)
+    backend.begin(counts)
+    log = []  # segments this rank added per batch
+
+    def exchange(ids):
+        if export:
+            backend.apply(torch.cat(_allgather_v(ids.to(device), group)))
+
+    n = len(seeds)
+    for b0 in range(0, n, bs):
+        nb = min(bs, n - b0)
+        b = slice_bounds(nb, world)
+        lo, hi = b0 + int(b[rank]), b0 + int(b[rank + 1])
+        added, ids = backend.scalp_batch(seeds[lo:hi], normals[lo:hi], export)
+        exchange(ids)
+        log.append(added)
+    n_scalp_batches = len(log)
+    nf = backend.field_begin() if (n > 0 and params.field_seeds > 0) else 0
+    for b0 in range(0, nf, bs):
+        nb = min(bs, nf - b0)
+        b = slice_bounds(nb, world)
+        added, ids = backend.field_batch(b0 + int(b[rank]), int(b[rank + 1] - b[rank]), export)
+        exchange(ids)
+        log.append(added)
+    offsets, verts, rooted, never = backend.end(counts)
+    # ---- global order: batch by batch, rank by rank (each rank's slice is contiguous)
+    logs = _allgather_v(torch.tensor(log, dtype=torch.int64, device=device), group)
+    nev = torch.tensor([never], dtype=torch.int64, device=device)
+    dist.all_reduce(nev, group=group)
+    lens = torch.as_tensor(np.diff(offsets), dtype=torch.int64, device=device)
+    all_lens = _allgather_v(lens, group)
+    all_verts = _allgather_v(torch.as_tensor(verts.reshape(-1), device=device), group)
+    all_root = _allgather_v(torch.as_tensor(rooted.astype(np.uint8), device=device), group)
+    if rank != 0:
+        return None
+    per_rank = []
+    for r in range(world):
+        ln = all_lens[r].cpu().numpy()
+        off = np.zeros(len(ln) + 1, np.int64)
+        np.cumsum(ln, out=off[1:])
+        per_rank.append((off, all_verts[r].cpu().numpy().reshape(-1, 3),
+                         all_root[r].cpu().numpy().astype(bool), logs[r].cpu().numpy()))
+    cursor = [0] * world
+    parts_v, parts_len, parts_root = [], [], []
+    n_scalp_segs = 0
+    for bi in range(len(log)):
+        for r in range(world):
+            off, v, ro, lg = per_rank[r]
+            k0, k1 = cursor[r], cursor[r] + int(lg[bi])
+            cursor[r] = k1
+            parts_v.append(v[off[k0]:off[k1]])
+            parts_len.append(np.diff(off[k0:k1 + 1]))
+            parts_root.append(ro[k0:k1])
+            if bi < n_scalp_batches:
+                n_scalp_segs += k1 - k0
+    lens_all = np.concatenate(parts_len) if parts_len else np.zeros(0, np.int64)
+    offsets_all = np.zeros(len(lens_all) + 1, np.int64)
+    np.cumsum(lens_all, out=offsets_all[1:])
+    verts_all = np.concatenate(parts_v) if parts_v else np.zeros((0, 3))
+    rooted_all = np.concatenate(parts_root) if parts_root else np.zeros(0, bool)
+    report = {"n_seeds": int(n), "n_segments": int(len(lens_all)),
+              "n_never_entered": int(nev.item())}
+    if n == 0:
+        report["warning"] = "no scalp seeds; nothing to trace"
+    else:
+        report["n_scalp_segments"] = int(n_scalp_segs)
+    return offsets_all, verts_all, rooted_all, report
+
+
 def gather_to_root(offsets_global, verts, entered, info: ShardInfo, group=None, device="cpu",
                    root=0):
     """Concatenate every rank's CSR on ``root`` (pad-to-max all-gather; NCCL has no gatherv).

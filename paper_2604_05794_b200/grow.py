@@ -93,6 +93,86 @@ def init_guide_strands_csr(seeds, normals, vol, params):
     return offsets, verts, rooted.astype(bool), report
 
 
+class DeviceGrowSession:
+    """Batch-level steps of the device driver (C ABI phg_grow_begin .. phg_grow_end).
+
+    The backend of dist.init_guide_strands_multirank on a GPU: seeds in, exported commit
+    ids out as CUDA tensors (for an NCCL all-gather), ids of every rank applied back in.
+    """
+
+    def __init__(self, vol, params, device=None):
+        import torch
+
+        self.torch = torch
+        self.device = device or torch.device("cuda", torch.cuda.current_device())
+        self.lib = _native.load()
+        self.vol = vol
+        self.params = params
+        self.field = field_for(vol)
+        self.tracer = _tracer()
+        self._p = _native.params_struct(params)
+        self._g = GrowParams(int(params.batch_size), int(params.occupancy_cap),
+                             int(params.field_seeds), 0)
+        near = _nearest_occupied_map(vol) if float(params.steer) > 0 else None
+        self.field.set_near(near)
+
+    def _ck(self, rc, what):
+        _native.check(rc, what)
+
+    def begin(self, counts):
+        self._ck(self.lib.phg_grow_begin(self.tracer.handle, self.field.handle,
+                                         ctypes.byref(self._p), ctypes.byref(self._g),
+                                         counts.ctypes.data, None), "phg_grow_begin")
+
+    def _ids(self, n):
+        ids = self.torch.empty(max(int(n), 1), dtype=self.torch.int32, device=self.device)[:n]
+        self._ck(self.lib.phg_grow_commits(self.tracer.handle, ids.data_ptr() if n else None,
+                                           None), "phg_grow_commits")
+        return ids
+
+    def scalp_batch(self, seeds, normals, export):
+        seeds = np.ascontiguousarray(seeds, np.float64)
+        normals = np.ascontiguousarray(normals, np.float64)
+        out = (ctypes.c_int64 * 2)()
+        n = len(seeds)
+        self._ck(self.lib.phg_grow_scalp_batch(self.tracer.handle,
+                                               seeds.ctypes.data if n else None,
+                                               normals.ctypes.data if n else None, n,
+                                               int(export), out, None), "phg_grow_scalp_batch")
+        return int(out[0]), (self._ids(out[1]) if export else None)
+
+    def field_begin(self):
+        nf = ctypes.c_int64()
+        self._ck(self.lib.phg_grow_field_begin(self.tracer.handle, ctypes.byref(nf), None),
+                 "phg_grow_field_begin")
+        return int(nf.value)
+
+    def field_batch(self, first, nb, export):
+        out = (ctypes.c_int64 * 2)()
+        self._ck(self.lib.phg_grow_field_batch(self.tracer.handle, int(first), int(nb),
+                                               int(export), out, None), "phg_grow_field_batch")
+        return int(out[0]), (self._ids(out[1]) if export else None)
+
+    def apply(self, ids):
+        n = int(ids.numel())
+        self._ck(self.lib.phg_grow_apply(self.tracer.handle, ids.data_ptr() if n else None, n,
+                                         None), "phg_grow_apply")
+
+    def end(self, counts):
+        nseg, nv = ctypes.c_int64(), ctypes.c_int64()
+        rep = (ctypes.c_int64 * 4)()
+        self._ck(self.lib.phg_grow_end(self.tracer.handle, counts.ctypes.data, ctypes.byref(nseg),
+                                       ctypes.byref(nv), rep, None), "phg_grow_end")
+        offsets = np.empty(nseg.value + 1, np.int64)
+        verts = np.empty((nv.value, 3))
+        rooted = np.empty(nseg.value, np.uint8)
+        self._ck(self.lib.phg_grow_fetch(self.tracer.handle, offsets.ctypes.data,
+                                         verts.ctypes.data if nv.value else None,
+                                         rooted.ctypes.data if nseg.value else None, None),
+                 "phg_grow_fetch")
+        return offsets, verts, rooted.astype(bool), int(rep[0])
+
+
 def init_guide_strands(scalp, vol, params, workers=1):
     """GPU drop-in for strandkit.phg.init_guide_strands (phg.py:210-260).
 
