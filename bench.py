@@ -296,9 +296,10 @@ def run_ours(args):
     if not args.no_e2e:
         e2e = e2e_leg(args, tracer, field, params, s_host, d_host, per_rank, ws, dev, steps_per_trace)
 
-    driver = None
+    driver = a9 = None
     if not args.no_driver and ws == 1:
         driver = driver_leg(cfg, field, s_host, d_host, dev)
+        a9 = a9_leg()
 
     kernel_ms = float(np.mean(kern_ms))
     peak, peak_kind = measured_peak()
@@ -339,7 +340,7 @@ def run_ours(args):
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": "trace_kernel", "kernel_ms": kernel_ms,
                          "bytes_per_step": BYTES_PER_STEP, "peak_source": peak_kind},
-            "cpu_baseline": cpu, "e2e": e2e, "clocks": clk, "driver": driver,
+            "cpu_baseline": cpu, "e2e": e2e, "clocks": clk, "driver": driver, "a9": a9,
             "gpu_launches": args.steps * phg.LAUNCHES_PER_TRACE,
         }
         print(json.dumps(line), flush=True)
@@ -393,6 +394,45 @@ def driver_leg(cfg, field, s_host, d_host, dev, repeats=2):
             "device_ms": min(dev_ms),
             "note": "seconds = wall clock incl. vol.counts H2D/D2H and the pageable host CSR "
                     "copy; device_ms = CUDA-event window of the device work alone"}
+
+
+def a9_leg(repeats=3):
+    """The reference's A9 scene (tests/golden/a9_scene.npz, written by the reference's own scene
+    pipeline): init_guide_strands and the full grow() on the device, host numpy in and out,
+    against the only published PHG timing (init_guide_strands, 1 worker: 2.70 s,
+    pkg/test_output.txt:28-34)."""
+    from types import SimpleNamespace
+
+    from paper_2604_05794_b200 import grow, link
+    from paper_2604_05794_b200.phg import PhgParams
+    from paper_2604_05794_b200.volume import OOVolume
+
+    z = np.load(os.path.join(ROOT, "tests", "golden", "a9_scene.npz"))
+    p = json.loads(str(z["params"]))
+    p.update(json.loads(str(z["link_params"])))
+    params = PhgParams(**{k: v for k, v in p.items() if k in PhgParams.__dataclass_fields__})
+    vol = OOVolume.empty(z["origin"], float(z["voxel_size"]), z["occ"].shape)
+    vol.occ, vol.ori = z["occ"], z["ori"]
+    scalp = SimpleNamespace(seeds=z["seeds"], seed_normals=z["dirs"],
+                            vertices=z["scalp_vertices"])
+    t_init, t_grow = [], []
+    for _ in range(repeats):
+        vol.counts[:] = 0
+        t0 = time.perf_counter()
+        segs, _ = grow.init_guide_strands(scalp, vol, params)
+        t_init.append(time.perf_counter() - t0)
+        vol.counts[:] = 0
+        t0 = time.perf_counter()
+        sset, _ = link.grow(scalp, vol, params)
+        t_grow.append(time.perf_counter() - t0)
+    ref_here = z["reference_seconds_here"].tolist()
+    return {"what": "reference A9 scene (4000 scalp + 4000 field seeds), host arrays in/out",
+            "init_guide_strands_s": min(t_init), "grow_s": min(t_grow),
+            "segments": len(segs), "strands": len(sset),
+            "published_reference_init_s": 2.70,
+            "reference_in_build_container_s": {"init_guide_strands": ref_here[0],
+                                               "grow": ref_here[1]},
+            "speedup_vs_published_init": 2.70 / min(t_init)}
 
 
 def sweep_variants(args, step, tracer, flush):

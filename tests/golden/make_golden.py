@@ -381,6 +381,73 @@ def link_cases():
         print(f"grow_{name} strands={len(sset)} report={rep}")
 
 
+def _digest(*arrays):
+    import hashlib
+
+    h = hashlib.sha256()
+    for a in arrays:
+        a = np.ascontiguousarray(a)
+        h.update(str(a.dtype).encode() + str(a.shape).encode())
+        h.update(a.tobytes())
+    return h.hexdigest()
+
+
+def a9_case():
+    """The reference's A9 scene (test_acceptance.py:302-334, conftest.small_config): the only
+    published PHG timing (pkg/test_output.txt:28-34, 2.70 s at 1 worker).  Inputs are stored;
+    outputs as digests (the full result is ~14 MB)."""
+    import time
+
+    sys.path.insert(0, "/root/reference/pkg/tests")
+    from conftest import small_config  # the reference's own test configuration
+    from strandkit import pipeline
+    from strandkit import volume as vol_mod
+    from strandkit.scalp import sample_seeds
+
+    cfg = small_config()
+    _, gt, scalp, _ = pipeline.scene_from_config(cfg)
+    verts, tans = gt.all_vertices_tangents()
+    vol = vol_mod.voxelize(verts, tans, voxel_size=2.0)
+    vol_mod.fill_interior(vol, scalp, max_depth_mm=6.0)
+    params = phg.PhgParams(n_root=4000, field_seeds=4000)
+    sample_seeds(scalp, params.n_root, seed=7)
+    vol.counts[:] = 0
+    t0 = time.perf_counter()
+    segs, rep = phg.init_guide_strands(scalp, vol, params, workers=1)
+    t_init = time.perf_counter() - t0
+    seg_off = np.zeros(len(segs) + 1, np.int64)
+    seg_off[1:] = np.cumsum([len(s.vertices) for s in segs])
+    seg_v = np.concatenate([s.vertices for s in segs])
+    seg_r = np.array([s.rooted for s in segs], bool)
+    counts_after_init = vol.counts.copy()
+    vol.counts[:] = 0
+    t0 = time.perf_counter()
+    sset, grep = phg.grow(scalp, vol, params, workers=1)
+    t_grow = time.perf_counter() - t0
+    st = list(sset)
+    off = np.zeros(len(st) + 1, np.int64)
+    off[1:] = np.cumsum([len(s.vertices) for s in st])
+    src_code = {"traced": 0, "field": 1, "linked": 2, "attached": 3}
+    np.savez_compressed(
+        os.path.join(HERE, "a9_scene.npz"), origin=vol.origin,
+        voxel_size=np.float64(vol.voxel_size), occ=vol.occ, ori=vol.ori, seeds=scalp.seeds,
+        dirs=scalp.seed_normals, scalp_vertices=scalp.vertices, params=np.array(params_json(p=params)),
+        link_params=np.array(json.dumps({k: getattr(params, k) for k in (
+            "link_dist_mm", "link_angle_deg", "tangent_window", "smooth", "smooth_strength",
+            "smooth_iters", "step_mm", "attach_radius_mm")})),
+        init_digest=np.array(_digest(seg_off, seg_v, seg_r, counts_after_init)),
+        init_report=np.array(json.dumps(rep)),
+        init_steps=np.int64(len(seg_v) - len(segs)),
+        grow_digest=np.array(_digest(off, np.concatenate([s.vertices for s in st]),
+                                     np.concatenate([s.tangents for s in st]),
+                                     np.array([s.rooted for s in st], bool),
+                                     np.array([src_code[s.source] for s in st], np.uint8))),
+        grow_report=np.array(json.dumps({k: v for k, v in grep.items() if not k.startswith("t_")})),
+        reference_seconds_here=np.array([t_init, t_grow]))
+    print(f"a9: dims={vol.dims} segments={len(segs)} init {t_init:.2f}s grow {t_grow:.2f}s "
+          f"report={rep}")
+
+
 def io_cases():
     """Reference wire formats: STND (strands.py:63-69) and OOVL (volume.py:236-246)."""
     from strandkit.strands import StrandSet, write_strands
@@ -399,6 +466,6 @@ def io_cases():
 if __name__ == "__main__":
     only = sys.argv[1:]  # e.g. `driver` to regenerate only the driver fixtures
     for fn in (unit_cases, helix_case, analytic_cases, sampler_case, driver_cases, io_cases,
-               link_cases):
+               link_cases, a9_case):
         if not only or any(o in fn.__name__ for o in only):
             fn()
