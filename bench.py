@@ -296,10 +296,12 @@ def run_ours(args):
     if not args.no_e2e:
         e2e = e2e_leg(args, tracer, field, params, s_host, d_host, per_rank, ws, dev, steps_per_trace)
 
-    driver = a9 = None
+    driver = a9 = dropin = None
     if not args.no_driver and ws == 1:
         driver = driver_leg(cfg, field, s_host, d_host, dev)
         a9 = a9_leg()
+    if not args.no_e2e and ws == 1 and ori_host is not None:
+        dropin = dropin_leg(ori_host, occ_host, s_host, d_host, params)
 
     kernel_ms = float(np.mean(kern_ms))
     peak, peak_kind = measured_peak()
@@ -341,6 +343,7 @@ def run_ours(args):
                          "kernel": "trace_kernel", "kernel_ms": kernel_ms,
                          "bytes_per_step": BYTES_PER_STEP, "peak_source": peak_kind},
             "cpu_baseline": cpu, "e2e": e2e, "clocks": clk, "driver": driver, "a9": a9,
+            "dropin": dropin,
             "gpu_launches": args.steps * phg.LAUNCHES_PER_TRACE,
         }
         print(json.dumps(line), flush=True)
@@ -394,6 +397,34 @@ def driver_leg(cfg, field, s_host, d_host, dev, repeats=2):
             "device_ms": min(dev_ms),
             "note": "seconds = wall clock incl. vol.counts H2D/D2H and the pageable host CSR "
                     "copy; device_ms = CUDA-event window of the device work alone"}
+
+
+def dropin_leg(ori_host, occ_host, s_host, d_host, params, repeats=2):
+    """The reference-facing call itself: phg.trace_batch_csr / phg.trace_batch with pageable
+    numpy arrays in and out (what strandkit callers get after install())."""
+    from types import SimpleNamespace
+
+    from paper_2604_05794_b200 import phg, synth
+
+    vol = SimpleNamespace(origin=np.zeros(3), voxel_size=synth.VOXEL_MM, dims=occ_host.shape,
+                          occ=occ_host, ori=ori_host)
+    off, verts, ent = phg.trace_batch_csr(vol, s_host[:1000], d_host[:1000], params)  # warm
+    t_csr, t_list = [], []
+    for _ in range(repeats):
+        t0 = time.perf_counter()
+        off, verts, ent = phg.trace_batch_csr(vol, s_host, d_host, params)
+        t_csr.append(time.perf_counter() - t0)
+    steps = int(len(verts) - len(ent))
+    del off, verts, ent
+    t0 = time.perf_counter()
+    out = phg.trace_batch(vol, s_host, d_host, params)
+    t_list.append(time.perf_counter() - t0)
+    del out
+    return {"what": "phg.trace_batch_csr / trace_batch (drop-in), pageable numpy in and out",
+            "csr_s": min(t_csr), "csr_steps_per_s": steps / min(t_csr),
+            "list_s": t_list[0], "list_steps_per_s": steps / t_list[0],
+            "note": "list_s includes building the reference's list of (vertices, entered) "
+                    "tuples (one numpy view per strand)"}
 
 
 def a9_leg(repeats=3):

@@ -13,7 +13,8 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
-SRCS = [os.path.join(HERE, "csrc", f) for f in ("phg_trace.cu", "phg_grow.cu", "phg_link.cu", "phg_io.cu")]
+SRCS = [os.path.join(HERE, "csrc", f)
+        for f in ("phg_trace.cu", "phg_grow.cu", "phg_link.cu", "phg_io.cu", "phg_copy.cu")]
 HDRS = [os.path.join(HERE, "csrc", "phg_core.cuh")]
 OUT = os.path.join(HERE, "libphg_b200.so")
 

@@ -779,8 +779,7 @@ phg_status phg_grow_end(phg_ctx* c, uint16_t* counts, int64_t* n_segments, int64
     uint16_t* dst16 = counts_dev ? counts : c->live_stage.as<uint16_t>();
     u32_to_u16<<<grid_for(V, 256, num_sms() * 16), 256, 0, st>>>(S.counts, dst16, V);
     PHG_CUDA(cudaGetLastError());
-    if (!counts_dev)
-        PHG_CUDA(cudaMemcpyAsync(counts, dst16, (size_t)V * 2, cudaMemcpyDeviceToHost, st));
+    if (!counts_dev) PHG_TRY(copy_d2h(counts, dst16, (size_t)V * 2, st));
     unsigned long long never = 0;
     PHG_CUDA(cudaMemcpyAsync(&never, S.misc.p, 8, cudaMemcpyDeviceToHost, st));
     PHG_TRY(ensure_output(G, 0, 0));
@@ -845,9 +844,10 @@ phg_status phg_grow_fetch(phg_ctx* c, int64_t* offsets, double* verts, uint8_t* 
     if (offsets)
         PHG_CUDA(cudaMemcpyAsync(offsets, c->g_out_off.p, (size_t)(c->grow_segs + 1) * 8,
                                  cudaMemcpyDefault, st));
-    if (verts && c->grow_verts)
-        PHG_CUDA(cudaMemcpyAsync(verts, c->g_out_verts.p, (size_t)c->grow_verts * 24,
-                                 cudaMemcpyDefault, st));
+    if (verts && c->grow_verts) {
+        PHG_CUDA(cudaStreamSynchronize(st));
+        PHG_TRY(copy_d2h(verts, c->g_out_verts.p, (size_t)c->grow_verts * 24, st));
+    }
     if (rooted && c->grow_segs)
         PHG_CUDA(cudaMemcpyAsync(rooted, c->g_out_rooted.p, (size_t)c->grow_segs,
                                  cudaMemcpyDefault, st));

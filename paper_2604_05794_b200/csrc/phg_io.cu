@@ -89,7 +89,7 @@ phg_status phg_stnd_encode(const int64_t* offsets, const double* verts, int64_t 
     stnd_encode_kernel<<<grid_for(std::max<long long>(n_strands, 1) * 32, 256, num_sms() * 16), 256,
                          0, st>>>((const long long*)d_off, (const double*)d_v, n_strands, d_out);
     PHG_CUDA(cudaGetLastError());
-    if (!out_dev) PHG_CUDA(cudaMemcpyAsync(out, d_out, bytes, cudaMemcpyDeviceToHost, st));
+    if (!out_dev) PHG_TRY(copy_d2h(out, d_out, bytes, st));
     PHG_CUDA(cudaStreamSynchronize(st));
     return PHG_OK;
 }
