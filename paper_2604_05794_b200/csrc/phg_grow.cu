@@ -598,22 +598,47 @@ phg_status field_batch(GrowCtx& G, long long first, long long nb, bool export_co
     const double* dir = c->g_fdir.as<double>() + 3 * first;
     const size_t rs = row_stride_doubles(S.p.max_vertices);
     PHG_TRY(set_cap_plane(G));
-    PHG_TRY(trace_core(c, S.f, &S.p, pos, dir, nb, S.strict ? S.counts : nullptr, G.st));
-    swap_buf(c->slab, c->g_slab2);  // keep the forward trace aside
-    swap_buf(c->keep, c->g_keep2);
-    swap_buf(c->entered, c->g_ent2);
-    PHG_TRY(c->g_neg_dir.ensure((size_t)nb * 24));
-    double* ndir = c->g_neg_dir.as<double>();
-    negate_kernel<<<grid_for(nb * 3, 256, num_sms() * 16), 256, 0, G.st>>>(dir, ndir, nb * 3);
-    PHG_CUDA(cudaGetLastError());
-    if (!S.strict) PHG_TRY(set_cap_plane(G));  // identical plane: no commits in between
-    PHG_TRY(trace_core(c, S.f, &S.p, pos, ndir, nb, S.strict ? S.counts : nullptr, G.st));
-    const double* slab_f = c->g_slab2.as<double>();
-    const long long* keep_f = c->g_keep2.as<long long>();
-    const uint8_t* ent_f = c->g_ent2.as<uint8_t>();
-    const double* slab_b = c->slab.as<double>();
-    const long long* keep_b = c->keep.as<long long>();
-    const uint8_t* ent_b = c->entered.as<uint8_t>();
+    const double *slab_f, *slab_b;
+    const long long *keep_f, *keep_b;
+    const uint8_t *ent_f, *ent_b;
+    if (!S.strict) {
+        // relaxed mode: +d and -d see the same frozen plane (no commits in between), so both
+        // directions run as ONE launch of 2*nb seeds: rows [0, nb) forward, [nb, 2nb) backward
+        PHG_TRY(c->g_neg_dir.ensure((size_t)nb * 24 * 4));
+        double* pos2 = c->g_neg_dir.as<double>();
+        double* dir2 = pos2 + 6 * nb;
+        PHG_CUDA(cudaMemcpyAsync(pos2, pos, (size_t)nb * 24, cudaMemcpyDeviceToDevice, G.st));
+        PHG_CUDA(cudaMemcpyAsync(pos2 + 3 * nb, pos, (size_t)nb * 24, cudaMemcpyDeviceToDevice,
+                                 G.st));
+        PHG_CUDA(cudaMemcpyAsync(dir2, dir, (size_t)nb * 24, cudaMemcpyDeviceToDevice, G.st));
+        negate_kernel<<<grid_for(nb * 3, 256, num_sms() * 16), 256, 0, G.st>>>(dir, dir2 + 3 * nb,
+                                                                                nb * 3);
+        PHG_CUDA(cudaGetLastError());
+        PHG_TRY(trace_core(c, S.f, &S.p, pos2, dir2, 2 * nb, nullptr, G.st));
+        slab_f = c->slab.as<double>();
+        slab_b = slab_f + (size_t)nb * rs;
+        keep_f = c->keep.as<long long>();
+        keep_b = keep_f + nb;
+        ent_f = c->entered.as<uint8_t>();
+        ent_b = ent_f + nb;
+    } else {
+        // strict: the -d trace sees the counts the +d trace committed (phg.py:283, :291-292)
+        PHG_TRY(trace_core(c, S.f, &S.p, pos, dir, nb, S.counts, G.st));
+        swap_buf(c->slab, c->g_slab2);  // keep the forward trace aside
+        swap_buf(c->keep, c->g_keep2);
+        swap_buf(c->entered, c->g_ent2);
+        PHG_TRY(c->g_neg_dir.ensure((size_t)nb * 24));
+        double* ndir = c->g_neg_dir.as<double>();
+        negate_kernel<<<grid_for(nb * 3, 256, num_sms() * 16), 256, 0, G.st>>>(dir, ndir, nb * 3);
+        PHG_CUDA(cudaGetLastError());
+        PHG_TRY(trace_core(c, S.f, &S.p, pos, ndir, nb, S.counts, G.st));
+        slab_f = c->g_slab2.as<double>();
+        keep_f = c->g_keep2.as<long long>();
+        ent_f = c->g_ent2.as<uint8_t>();
+        slab_b = c->slab.as<double>();
+        keep_b = c->keep.as<long long>();
+        ent_b = c->entered.as<uint8_t>();
+    }
     BatchScratch B;
     PHG_TRY(batch_scratch(G, nb, B));
     join_select_kernel<<<grid_for(nb, 256), 256, 0, G.st>>>(keep_f, ent_f, keep_b, ent_b, nb,
