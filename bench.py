@@ -66,14 +66,37 @@ def measured_peak():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic():
-    """Per-launch DRAM bytes of the trace kernel from the committed ncu summary, if any."""
+def ncu_summary():
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_trace_summary.json")) as f:
-            d = json.load(f)
-        return d.get("dram_bytes_per_launch"), d.get("steps_per_launch")
+            return json.load(f)
     except Exception:  # noqa: BLE001
-        return None, None
+        return {}
+
+
+def ncu_traffic():
+    """Per-launch DRAM bytes of the trace kernel from the committed ncu summary, if any."""
+    d = ncu_summary()
+    return d.get("dram_bytes_per_launch"), d.get("steps_per_launch")
+
+
+def binding_resource():
+    """What actually bounds the trace kernel per the committed ncu capture: the gathers are
+    L1/L2-resident, so DRAM is far from busy; issue slots and the fp64 pipe are the limits."""
+    m = ncu_summary().get("metrics", {})
+
+    def pct(k):
+        try:
+            return float(m[k][0]) / 100.0
+        except Exception:  # noqa: BLE001
+            return None
+
+    return {"issue_active": pct("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+            "fp64_pipe": pct("sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active"),
+            "l1_wavefronts": pct("l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed"),
+            "dram": pct("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"),
+            "inst_per_step": ncu_summary().get("inst_per_step"),
+            "source": "profiles/ncu_trace_summary.json (ncu --set full, C3)"}
 
 
 class ClockSampler:
@@ -341,7 +364,8 @@ def run_ours(args):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": "trace_kernel", "kernel_ms": kernel_ms,
-                         "bytes_per_step": BYTES_PER_STEP, "peak_source": peak_kind},
+                         "bytes_per_step": BYTES_PER_STEP, "peak_source": peak_kind,
+                         "binding": binding_resource()},
             "cpu_baseline": cpu, "e2e": e2e, "clocks": clk, "driver": driver, "a9": a9,
             "dropin": dropin,
             "gpu_launches": args.steps * phg.LAUNCHES_PER_TRACE,
