@@ -18,8 +18,19 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "l1tex__throughput.avg.pct_of_peak_sustained_active",
         "l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed",
         "lts__throughput.avg.pct_of_peak_sustained_elapsed",
-        "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"]
+        "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
+        "l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum",
+        "l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum",
+        "l1tex__t_sectors_pipe_lsu_mem_global_op_st.sum",
+        "l1tex__t_requests_pipe_lsu_mem_global_op_st.sum"]
 SCALE = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0}
+
+
+def _ratio(v, col, a, b):
+    try:
+        return float(v[col[a]].replace(",", "")) / float(v[col[b]].replace(",", ""))
+    except (KeyError, ValueError, ZeroDivisionError):
+        return None
 
 
 def main(rep, out, label, cmd, steps):
@@ -46,6 +57,14 @@ def main(rep, out, label, cmd, steps):
          "steps_per_launch": steps, "dram_bytes_per_launch": dr + dw, "dram_read_bytes": dr,
          "dram_write_bytes": dw, "dram_bytes_per_step": (dr + dw) / steps,
          "inst_per_step": float(v[col["smsp__inst_executed.sum"]]) * 32 / steps,
+         # sector efficiency: 32-B sectors touched per warp-level request.  A 16-B/lane corner
+         # gather touches 16 sectors when the 32 lanes read 32 distinct contiguous voxels; fewer
+         # means lanes share voxels (Morton-ordered neighbours); the staged vertex stores touch
+         # 32 sectors per request (one row per lane) but always whole sectors
+         "ld_sectors_per_request": _ratio(v, col, "l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum",
+                                          "l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum"),
+         "st_sectors_per_request": _ratio(v, col, "l1tex__t_sectors_pipe_lsu_mem_global_op_st.sum",
+                                          "l1tex__t_requests_pipe_lsu_mem_global_op_st.sum"),
          "stalls_per_issue": dict(sorted(stalls.items(), key=lambda kv: -kv[1])), "metrics": m}
     with open(out, "w") as f:
         json.dump(d, f, indent=1)
