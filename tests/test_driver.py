@@ -105,6 +105,53 @@ def test_device_driver_prefilled_counts_and_uint16_wrap(oracle_c):
     assert (counts < init).any()  # some voxel really wrapped
 
 
+def _driver_vs_oracle(kind, n, nseeds, key, radius_frac=0.4, **pkw):
+    from oracle import phg_driver_np as dn
+    from paper_2604_05794_b200 import grow, synth
+    from paper_2604_05794_b200.volume import OOVolume
+
+    ori, occ = synth.make_field(kind, n, "cpu")
+    ori, occ = ori.numpy(), occ.numpy()
+    seeds, dirs = synth.disk_seeds(n, nseeds, key, radius_frac=radius_frac)
+    params = _params(pkw)
+    vol = OOVolume.empty((0, 0, 0), synth.VOXEL_MM, occ.shape)
+    vol.occ, vol.ori = occ, ori
+    segs, rep = grow.init_guide_strands(SimpleNamespace(seeds=seeds, seed_normals=dirs), vol,
+                                        params)
+    counts = np.zeros(occ.shape, np.uint16)
+    near = near_map(occ) if params.steer > 0 else None
+    out, rep_o = dn.init_guide(np.zeros(3), synth.VOXEL_MM, occ, ori, counts, seeds, dirs, params,
+                               near_occ=near)
+    assert rep == rep_o
+    assert np.array_equal(vol.counts, counts)
+    off, verts, rooted = _csr([(s.vertices, s.rooted) for s in segs])
+    off_o, verts_o, rooted_o = _csr(out)
+    assert np.array_equal(off, off_o) and np.array_equal(rooted, rooted_o)
+    assert np.array_equal(verts, verts_o)
+    return rep
+
+
+@pytest.mark.gpu
+def test_device_driver_long_segments_global_hash_tables(oracle_c):
+    """max_vertices 2500 with small steps: joined field segments exceed the shared-memory
+    hash table, exercising the global-memory commit path (csrc/phg_grow.cu)."""
+    rep = _driver_vs_oracle("wavy", 48, 600, 51, step_mm=0.05, max_vertices=2500,
+                            batch_size=200, occupancy_cap=3, field_seeds=300)
+    assert rep["n_segments"] > rep["n_scalp_segments"] > 0
+
+
+@pytest.mark.gpu
+def test_device_driver_strict_at_scale(oracle_c):
+    _driver_vs_oracle("curly", 48, 1500, 52, strict=True, batch_size=500, field_seeds=400,
+                      max_vertices=150)
+
+
+@pytest.mark.gpu
+def test_device_driver_steer_at_scale(oracle_c):
+    _driver_vs_oracle("sparse", 48, 2000, 53, radius_frac=0.45, steer=0.4, coast_steps=6,
+                      batch_size=700, occupancy_cap=2, field_seeds=800)
+
+
 @pytest.mark.gpu
 def test_device_driver_matches_oracle_at_scale(oracle_c):
     """128^3 curly field, 20k scalp seeds in 5 batches with cap 4, 8k field seeds."""
