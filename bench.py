@@ -46,9 +46,17 @@ def parse():
     ap.add_argument("--cpu-sample", type=int, default=0, help="seeds in the CPU sample")
     ap.add_argument("--sweep", action="store_true", help="time every trace-kernel variant")
     ap.add_argument("--no-driver", action="store_true", help="skip the batch-driver leg")
+    ap.add_argument("--sweep-sizes", action="store_true",
+                    help="one-lane vs 8-lane trace kernel across launch sizes")
     ap.add_argument("--e2e-chunk", type=int, default=0,
                     help="seeds per chunk of the pipelined host path (0: library default)")
     return ap.parse_args()
+
+
+def _native_variants():
+    from paper_2604_05794_b200 import _native
+
+    return int(_native.load().phg_num_variants())
 
 
 def dist_env():
@@ -279,6 +287,10 @@ def run_ours(args):
     if args.sweep:
         sweep_variants(args, step, tracer, flush)
         return
+    if args.sweep_sizes:
+        nv = _native_variants()
+        sweep_launch_sizes(field, s_dev, d_dev, params, tracer, stream, [0, nv - 1])
+        return
 
     for _ in range(args.warmup):
         flush.zero_()
@@ -488,6 +500,35 @@ def a9_leg(repeats=3):
             "reference_in_build_container_s": {"init_guide_strands": ref_here[0],
                                                "grow": ref_here[1]},
             "speedup_vs_published_init": 2.70 / min(t_init)}
+
+
+def sweep_launch_sizes(field, s_dev, d_dev, params, tracer, stream, variants):
+    """Trace-kernel time vs launch size for the given variants (small-batch regime: the
+    reference's default deferred-commit batches are 16384 seeds); checks byte-identity."""
+    import torch
+
+    from paper_2604_05794_b200 import phg
+
+    for n in (1024, 4096, 16384, 32768, 65536, 131072, 262144):
+        ref = None
+        row = {"seeds": n}
+        for v in variants:
+            os.environ["PHG_VARIANT"] = str(v)
+            for _ in range(2):
+                off, verts, _ = phg.trace_device(field, s_dev[:n], d_dev[:n], params,
+                                                 tracer=tracer, stream=stream)
+            ms = []
+            for _ in range(3):
+                off, verts, _ = phg.trace_device(field, s_dev[:n], d_dev[:n], params,
+                                                 tracer=tracer, stream=stream)
+                ms.append(tracer.last_kernel_ms()[0])
+            torch.cuda.synchronize()
+            same = ref is None or (torch.equal(ref[0], off) and torch.equal(ref[1], verts))
+            if ref is None:
+                ref = (off.clone(), verts.clone())
+            row[tracer.last_variant()] = {"kernel_ms": min(ms), "identical": bool(same)}
+        print(json.dumps(row), flush=True)
+    os.environ.pop("PHG_VARIANT", None)
 
 
 def sweep_variants(args, step, tracer, flush):
