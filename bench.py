@@ -288,8 +288,8 @@ def run_ours(args):
         sweep_variants(args, step, tracer, flush)
         return
     if args.sweep_sizes:
-        nv = _native_variants()
-        sweep_launch_sizes(field, s_dev, d_dev, params, tracer, stream, [0, nv - 1])
+        sweep_launch_sizes(field, s_dev, d_dev, params, tracer, stream,
+                           list(range(min(2, _native_variants()))))
         return
 
     for _ in range(args.warmup):

@@ -266,34 +266,6 @@ def test_device_api_matches_host_api(gpu):
     assert np.array_equal(e2.cpu().numpy().astype(bool), e)
 
 
-@pytest.fixture()
-def coop_variant(gpu, monkeypatch):
-    """Force the 8-lanes-per-strand trace kernel (the last compiled variant)."""
-    from paper_2604_05794_b200 import _native
-
-    monkeypatch.setenv("PHG_VARIANT", str(_native.load().phg_num_variants() - 1))
-    return gpu
-
-
-@pytest.mark.parametrize("path", [p for p in CASES if "strict" not in p],
-                         ids=lambda p: os.path.basename(p)[6:-4])
-def test_coop8_kernel_matches_reference_golden(coop_variant, path):
-    gpu = coop_variant
-    c = load_case(path)
-    off, v, ent = run_gpu(gpu, c)
-    assert gpu.phg._tracer().last_variant() in ("coop8", "")  # "" for zero seeds
-    assert np.array_equal(ent, c.entered)
-    assert csr_equal(off, v, c.offsets, c.verts)
-
-
-def test_coop8_kernel_divergent_and_capped(coop_variant, oracle_c):
-    vol, s, d, p = _config_case("sparse", 96, 3_000, 15, interior=3_000)
-    _compare_with_oracle(coop_variant, oracle_c, vol, s, d, p)
-    vol, s, d, p = _config_case("curly", 64, 5_000, 16)
-    cap = np.random.Generator(np.random.Philox(key=3)).random(vol.occ.shape) < 0.02
-    _compare_with_oracle(coop_variant, oracle_c, vol, s, d, p, at_cap=cap)
-
-
 def test_pipelined_host_path_matches(gpu):
     """phg_trace_to_host (chunked, overlapped D2H) == phg_trace + phg_gather, any chunking."""
     torch = gpu.torch
