@@ -155,6 +155,23 @@ def test_nonempty_cap_plane_bit_exact(gpu, oracle_c):
     _compare_with_oracle(gpu, oracle_c, vol, s, d, p, at_cap=cap)
 
 
+def test_every_kernel_variant_bit_exact(gpu, oracle_c, monkeypatch):
+    """Each compiled trace-kernel variant (PHG_VARIANT) against the oracle, with and
+    without an at_cap plane, on the divergent sparse field."""
+    from paper_2604_05794_b200 import _native
+
+    vol, s, d, p = _config_case("sparse", 64, 1_500, 21, interior=1_500)
+    cap = np.random.Generator(np.random.Philox(key=5)).random(vol.occ.shape) < 0.02
+    tracer = gpu.phg._tracer()
+    names = []
+    for v in range(_native.load().phg_num_variants()):
+        monkeypatch.setenv("PHG_VARIANT", str(v))
+        for plane in (None, cap):
+            _compare_with_oracle(gpu, oracle_c, vol, s, d, p, at_cap=plane)
+        names.append(tracer.last_variant())
+    assert len(set(names)) == len(names), names
+
+
 def test_seed_order_does_not_change_results(gpu):
     """Locality ordering is scheduling only: seed i's strand is the same at any position."""
     vol, s, d, p = _config_case("sparse", 64, 6_000, 17, interior=1_000)
