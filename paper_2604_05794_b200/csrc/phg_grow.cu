@@ -244,12 +244,13 @@ __global__ void gather_joined_kernel(const double* __restrict__ slab_f,
 }
 
 // unvisited = argwhere(occ & (counts == 0)) (phg.py:266): flag per voxel
-__global__ void unvisited_flag_kernel(const float4* __restrict__ vox,
-                                      const uint32_t* __restrict__ counts, long long nvox,
-                                      uint8_t* __restrict__ flag) {
+__global__ void unvisited_flag_kernel(FieldView F, const uint32_t* __restrict__ counts,
+                                      long long nvox, uint8_t* __restrict__ flag) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nvox;
          i += (long long)gridDim.x * blockDim.x)
-        flag[i] = (vox[i].w != 0.0f && (counts[i] & 0xffffu) == 0u) ? 1 : 0;
+        flag[i] = (F.vox[vox_index_lin(F, (uint32_t)i)].w != 0.0f && (counts[i] & 0xffffu) == 0u)
+                      ? 1
+                      : 0;
 }
 
 // unvisited[np.linspace(0, U - 1, m).astype(np.int64)] (phg.py:269-271), numpy-exact:
@@ -283,7 +284,7 @@ __global__ void field_seed_kernel(FieldView F, const uint32_t* __restrict__ lin,
     pos[3 * k + 0] = F.ox + ((double)x + 0.5) * F.vs;
     pos[3 * k + 1] = F.oy + ((double)y + 0.5) * F.vs;
     pos[3 * k + 2] = F.oz + ((double)z + 0.5) * F.vs;
-    const float4 v = F.vox[l];
+    const float4 v = F.vox[vox_index(F, (int)x, (int)y, (int)z)];
     double ox = (double)v.x, oy = (double)v.y, oz = (double)v.z;
     const double n = nrm3(ox, oy, oz);
     keepf[k] = (n > 1e-9) ? 1 : 0;
@@ -536,7 +537,7 @@ phg_status field_begin(GrowCtx& G) {
     PHG_TRY(c->g_sel.ensure((size_t)V * 4));
     uint8_t* flags = c->g_flags.as<uint8_t>();
     uint32_t* unvisited = c->g_sel.as<uint32_t>();
-    unvisited_flag_kernel<<<grid_for(V, 256, num_sms() * 16), 256, 0, G.st>>>(F.vox, S.counts, V,
+    unvisited_flag_kernel<<<grid_for(V, 256, num_sms() * 16), 256, 0, G.st>>>(F, S.counts, V,
                                                                               flags);
     PHG_CUDA(cudaGetLastError());
     size_t tmp = 0;

@@ -44,7 +44,9 @@ __global__ void byte_popc_kernel(const uint8_t* __restrict__ bits, long long nby
 
 // voxel i is bit (7 - i%8) of byte i/8 (np.packbits, bitorder="big"); its ori is row
 // rank(i) = (set bits before byte i/8) + (set bits above it within the byte)
-__global__ void oovl_scatter_kernel(const uint8_t* __restrict__ bits,
+// Unoccupied voxels keep the zeros of the freshly cleared padded field (read_volume fills
+// their ori with 0, so the packing is the zeroed one whenever the payload is finite).
+__global__ void oovl_scatter_kernel(FieldView F, const uint8_t* __restrict__ bits,
                                     const unsigned long long* __restrict__ byte_rank,
                                     const float* __restrict__ ori, long long nvox,
                                     float4* __restrict__ out) {
@@ -54,9 +56,8 @@ __global__ void oovl_scatter_kernel(const uint8_t* __restrict__ bits,
         const int k = (int)(i & 7);
         if ((b >> (7 - k)) & 1u) {
             const unsigned long long r = byte_rank[i >> 3] + __popc(b >> (8 - k));
-            out[i] = make_float4(ori[3 * r], ori[3 * r + 1], ori[3 * r + 2], 1.0f);
-        } else {
-            out[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+            out[vox_index_lin(F, (uint32_t)i)] =
+                make_float4(ori[3 * r], ori[3 * r + 1], ori[3 * r + 2], occ_flag(true));
         }
     }
 }
@@ -100,8 +101,7 @@ phg_status phg_field_from_oovl(phg_field** out, const uint8_t* bits, const float
     if (!out || !bits || !origin || n_occ < 0)
         return fail(PHG_ERR_INVALID, "phg_field_from_oovl: null argument");
     *out = nullptr;
-    if (nx < 1 || ny < 1 || nz < 1 || (double)nx * ny * nz >= 4294967296.0)
-        return fail(PHG_ERR_INVALID, "phg_field_from_oovl: bad dims");
+    if (!field_dims_ok(nx, ny, nz)) return fail(PHG_ERR_INVALID, "phg_field_from_oovl: bad dims");
     if (!(voxel_size > 0) || !std::isfinite(voxel_size))
         return fail(PHG_ERR_INVALID, "phg_field_from_oovl: voxel_size must be positive");
     cudaStream_t st = as_stream(stream);
@@ -144,13 +144,14 @@ phg_status phg_field_from_oovl(phg_field** out, const uint8_t* bits, const float
     f->nz = nz;
     for (int k = 0; k < 3; ++k) f->origin[k] = origin[k];
     f->vs = voxel_size;
-    phg_status s = f->vox.ensure((size_t)V * sizeof(float4));
+    phg_status s = field_alloc_padded(f, st);
+    if (s == PHG_OK) s = field_check_finite(f, (const float*)d_ori, 3 * n_occ, st);
     if (s != PHG_OK) {
         delete f;
         return s;
     }
     oovl_scatter_kernel<<<grid_for(V, 256, num_sms() * 16), 256, 0, st>>>(
-        (const uint8_t*)d_bits, r, (const float*)d_ori, V, f->vox.as<float4>());
+        f->view(), (const uint8_t*)d_bits, r, (const float*)d_ori, V, f->vox.as<float4>());
     cudaError_t e = cudaGetLastError();
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) {
