@@ -254,6 +254,28 @@ def analytic_cases():
     save("curly32_strict", vol, seeds, dirs, p, out, counts_in=c0, counts_out=counts)
 
 
+def nonfinite_case():
+    """Non-finite orientations: NaN/inf in some unoccupied voxels, on occupied border voxels and
+    in a few occupied interior voxels.  The reference's masked weights still multiply them
+    (0 * NaN = NaN), so strands touching them change; the device must take its exact sampler."""
+    ori, occ = field_np("curly", 24)
+    rng = np.random.Generator(np.random.Philox(key=41))
+    ori = ori.copy()
+    empty = np.argwhere(~occ)
+    for i in rng.choice(len(empty), size=min(40, len(empty)), replace=False):
+        ori[tuple(empty[i])] = (np.nan, 0.5, -np.inf)
+    full = np.argwhere(occ)
+    border = full[(full == 0).any(axis=1) | (full == 23).any(axis=1)]
+    for i in rng.choice(len(border), size=min(10, len(border)), replace=False):
+        ori[tuple(border[i])] = (np.inf, np.nan, 0.0)
+    for i in rng.choice(len(full), size=5, replace=False):
+        ori[tuple(full[i])] = (np.nan, np.nan, np.nan)
+    vol = vol_of((0, 0, 0), synth.VOXEL_MM, occ, ori)
+    seeds, dirs = synth.disk_seeds(24, 300, 42, radius_frac=0.48)
+    p = phg.PhgParams(field_seeds=0, max_vertices=120)
+    save("curly24_nonfinite", vol, seeds, dirs, p, phg.trace_batch(vol, seeds, dirs, p))
+
+
 def sampler_case():
     ori, occ = field_np("sparse", 24, sparse_sigma=1.5)
     vol = vol_of((-5.0, 3.0, 1.0), 1.5, occ, ori)
@@ -465,7 +487,7 @@ def io_cases():
 
 if __name__ == "__main__":
     only = sys.argv[1:]  # e.g. `driver` to regenerate only the driver fixtures
-    for fn in (unit_cases, helix_case, analytic_cases, sampler_case, driver_cases, io_cases,
-               link_cases, a9_case):
+    for fn in (unit_cases, helix_case, analytic_cases, nonfinite_case, sampler_case, driver_cases,
+               io_cases, link_cases, a9_case):
         if not only or any(o in fn.__name__ for o in only):
             fn()
