@@ -564,7 +564,8 @@ def sweep_variants(args, step, tracer, flush):
         else:
             same = bool(torch.equal(ref[0], off) and torch.equal(ref[1], verts))
         acc = tracer.last_steps()
-        print(json.dumps({"variant": v, "name": tracer.last_variant(), "kernel_ms": min(ms),
+        print(json.dumps({"variant": v, "name": tracer.last_variant(),
+                          "sampler": tracer.last_sampler(), "kernel_ms": min(ms),
                           "kernel_ms_all": ms, "gsteps_per_s": acc / min(ms) / 1e6,
                           "identical_to_variant0": same}), flush=True)
         del off, verts

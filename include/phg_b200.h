@@ -212,6 +212,10 @@ phg_status phg_last_kernel_ms(phg_ctx* c, float* trace_ms, float* total_ms);
 /* name of the trace-kernel variant the last trace used (env PHG_VARIANT=<index> selects one;
  * all variants are bit-identical) and the number of compiled variants */
 const char* phg_last_variant(phg_ctx* c);
+/* sampler form the last trace used, chosen per field (all bit-identical): "exact" (a field
+ * with non-finite ori, steering, strict mode), "fast" (all ori finite: zeroed padded field),
+ * "fast-pow2" (and a power-of-two voxel size) */
+const char* phg_last_sampler(phg_ctx* c);
 /* device self-test of the arithmetic building blocks: runs n randomized and edge-case
  * operand pairs through the kernel's shared-reciprocal division and the compiler's own
  * IEEE division and reports how many results differ bitwise (must be 0) */

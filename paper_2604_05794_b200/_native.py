@@ -25,7 +25,8 @@ EXPORTS = (
     "phg_field_create", "phg_field_set_cap", "phg_field_set_near", "phg_field_destroy",
     "phg_field_info", "phg_ctx_create", "phg_ctx_destroy", "phg_trace", "phg_gather",
     "phg_last_steps", "phg_sample", "phg_last_error", "phg_abi_version", "phg_last_kernel_ms",
-    "phg_last_variant", "phg_num_variants", "phg_selftest", "phg_grow_init", "phg_grow_fetch",
+    "phg_last_variant", "phg_last_sampler", "phg_num_variants", "phg_selftest", "phg_grow_init",
+    "phg_grow_fetch",
     "phg_trace_to_host", "phg_stnd_encode", "phg_field_from_oovl", "phg_link", "phg_link_fetch",
     "phg_grow_begin", "phg_grow_scalp_batch", "phg_grow_field_begin", "phg_grow_field_batch",
     "phg_grow_commits", "phg_grow_apply", "phg_grow_end",
@@ -86,6 +87,7 @@ def _declare(lib):
         "phg_last_kernel_ms": (S, [VP, ctypes.POINTER(ctypes.c_float),
                                    ctypes.POINTER(ctypes.c_float)]),
         "phg_last_variant": (ctypes.c_char_p, [VP]),
+        "phg_last_sampler": (ctypes.c_char_p, [VP]),
         "phg_num_variants": (ctypes.c_int, []),
         "phg_selftest": (S, [I64, ctypes.c_uint64, ctypes.POINTER(I64), VP]),
         "phg_grow_init": (S, [VP, VP, ctypes.POINTER(Params), VP, VP, VP, I64, VP,

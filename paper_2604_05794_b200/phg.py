@@ -114,6 +114,10 @@ class Tracer:
     def last_variant(self):
         return self._lib.phg_last_variant(self.handle).decode()
 
+    def last_sampler(self):
+        """exact / fast / fast-pow2 / fast-pow2-s32 (chosen per field; all bit-identical)."""
+        return self._lib.phg_last_sampler(self.handle).decode()
+
     def last_kernel_ms(self):
         a, b = ctypes.c_float(), ctypes.c_float()
         _native.check(self._lib.phg_last_kernel_ms(self.handle, ctypes.byref(a), ctypes.byref(b)),

@@ -163,13 +163,37 @@ def test_every_kernel_variant_bit_exact(gpu, oracle_c, monkeypatch):
     vol, s, d, p = _config_case("sparse", 64, 1_500, 21, interior=1_500)
     cap = np.random.Generator(np.random.Philox(key=5)).random(vol.occ.shape) < 0.02
     tracer = gpu.phg._tracer()
-    names = []
+    names, samplers = [], set()
     for v in range(_native.load().phg_num_variants()):
         monkeypatch.setenv("PHG_VARIANT", str(v))
         for plane in (None, cap):
             _compare_with_oracle(gpu, oracle_c, vol, s, d, p, at_cap=plane)
         names.append(tracer.last_variant())
+        samplers.add(tracer.last_sampler())
     assert len(set(names)) == len(names), names
+    assert samplers == {"exact", "fast-pow2"}, samplers
+
+
+@pytest.mark.parametrize("kind,vs,nan,want", [
+    ("curly", 2.0, False, "fast-pow2"), ("curly", 1.7, False, "fast"),
+    ("sparse", 0.5, False, "fast-pow2"), ("wavy", 2.0, True, "exact")])
+def test_sampler_forms_bit_exact(gpu, oracle_c, kind, vs, nan, want):
+    """The per-field sampler choice (exact / fast / fast-pow2) on fields of each kind and
+    voxel size, against the oracle; one NaN ori anywhere selects the exact sampler."""
+    vol, s, d, p = _config_case(kind, 48, 600, 31, interior=600 if kind == "sparse" else 0)
+    ori = vol.ori.copy()
+    if nan:
+        ori[0, 0, 0] = (np.nan, 1.0, 0.0)
+    vol.ori, vol.voxel_size = ori, vs
+    s = s / synth_voxel() * vs
+    _compare_with_oracle(gpu, oracle_c, vol, s, d, p)
+    assert gpu.phg._tracer().last_sampler() == want
+
+
+def synth_voxel():
+    from paper_2604_05794_b200 import synth
+
+    return synth.VOXEL_MM
 
 
 def test_seed_order_does_not_change_results(gpu):
