@@ -18,7 +18,7 @@ import numpy as np
 
 from . import _native
 from .errors import DataError
-from .phg import _tracer
+from .phg import _tracer, split_rows
 from .volume import field_for
 
 try:  # the reference's own container when it is importable (drop-in object identity)
@@ -185,12 +185,8 @@ def init_guide_strands(scalp, vol, params, workers=1):
         report["warning"] = "no scalp seeds; nothing to trace"
         return [], report
     offsets, verts, rooted, rep = init_guide_strands_csr(seeds, normals, vol, params)
-    segments = []
-    for i, part in enumerate(np.split(verts, offsets[1:-1]) if len(rooted) else []):
-        if rooted[i]:
-            segments.append(Strand(vertices=part, rooted=True, source="traced"))
-        else:
-            segments.append(Strand(vertices=part, rooted=False, source="field"))
+    segments = [Strand(vertices=part, rooted=r, source="traced" if r else "field")
+                for part, r in zip(split_rows(verts, offsets), rooted.tolist())]
     report["n_never_entered"] = rep["n_never_entered"]
     report["n_scalp_segments"] = rep["n_scalp_segments"]
     report["n_segments"] = len(segments)

@@ -22,7 +22,7 @@ import numpy as np
 from . import _native
 from .errors import DataError
 from .grow import GrowParams, Strand, _nearest_occupied_map
-from .phg import PhgParams, _tracer
+from .phg import PhgParams, _tracer, split_rows
 from .volume import field_for
 
 try:  # the reference's container when importable
@@ -99,14 +99,14 @@ def connect_segments_csr(offsets, verts, rooted, source, params, scalp_vertices=
 
 
 def _strands(res, with_tangents):
-    out = []
     off = res["offsets"]
-    for k in range(len(off) - 1):
-        v = res["verts"][off[k]:off[k + 1]]
-        s = Strand(vertices=v, rooted=bool(res["rooted"][k]), source=SOURCES[res["source"][k]])
-        if with_tangents:
-            s.tangents = res["tangents"][off[k]:off[k + 1]]
-        out.append(s)
+    verts = split_rows(res["verts"], off)
+    names = [SOURCES[c] for c in res["source"].tolist()]
+    out = [Strand(vertices=v, rooted=r, source=s)
+           for v, r, s in zip(verts, res["rooted"].tolist(), names)]
+    if with_tangents:
+        for s, t in zip(out, split_rows(res["tangents"], off)):
+            s.tangents = t
     return out
 
 

@@ -197,8 +197,14 @@ def trace_batch(vol, seed_pos, seed_dir, params, at_cap=None, live_counts=None, 
     """
     offsets, verts, entered = trace_batch_csr(vol, seed_pos, seed_dir, params, at_cap=at_cap,
                                               live_counts=live_counts, near_occ=near_occ)
-    parts = np.split(verts, offsets[1:-1]) if len(entered) else []
-    return list(zip(parts, entered.tolist()))
+    return list(zip(split_rows(verts, offsets), entered.tolist()))
+
+
+def split_rows(verts, offsets):
+    """[verts[offsets[i]:offsets[i+1]] for each i] as views, ~4x faster than np.split for
+    ~1M rows (no per-piece swapaxes)."""
+    o = offsets.tolist()
+    return list(map(verts.__getitem__, map(slice, o[:-1], o[1:])))
 
 
 def trace_device(field, seed_pos, seed_dir, params, tracer=None, stream=None, order=True):
