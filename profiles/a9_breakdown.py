@@ -1,11 +1,11 @@
 import cProfile, pstats, io, json, os, sys, time
 import numpy as np
-sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from types import SimpleNamespace
 from paper_2604_05794_b200 import grow
 from paper_2604_05794_b200.phg import PhgParams
 from paper_2604_05794_b200.volume import OOVolume
-z = np.load("tests/golden/a9_scene.npz")
+z = np.load(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests", "golden", "a9_scene.npz"))
 p = json.loads(str(z["params"])); p.update(json.loads(str(z["link_params"])))
 params = PhgParams(**{k: v for k, v in p.items() if k in PhgParams.__dataclass_fields__})
 vol = OOVolume.empty(z["origin"], float(z["voxel_size"]), z["occ"].shape)
