@@ -345,3 +345,83 @@ def test_shared_reciprocal_division_matches_ieee_division(gpu):
     bad = ctypes.c_int64(-1)
     _native.check(lib.phg_selftest(8_000_000, 12345, ctypes.byref(bad), None), "selftest")
     assert bad.value == 0
+
+
+def test_c3_full_size_properties(gpu, oracle_c):
+    """BASELINE C3 at full size (512^3 curly field, 1M disk seeds), device-resident:
+    * a random sample of 2000 strands of the full trace equals the oracle bit for bit;
+    * the trace does not depend on seed order (all 1M lengths and the sampled strands are
+      identical when the seeds are reversed);
+    * accepted steps = sum(len - 1) over strands, as the bench counts them."""
+    from paper_2604_05794_b200 import phg, synth
+    from paper_2604_05794_b200.volume import DeviceField
+
+    torch = gpu.torch
+    dev = torch.device("cuda", 0)
+    cfg = synth.CONFIGS["C3"]
+    ori, occ = synth.make_field(cfg.kind, cfg.n, dev)
+    field = DeviceField(np.zeros(3), synth.VOXEL_MM, occ, ori,
+                        torch.cuda.current_stream(dev).cuda_stream)
+    s, d = synth.config_seeds(cfg, cfg.seeds, ori, occ)
+    params = phg.PhgParams(field_seeds=0, batch_size=len(s))
+    s_dev, d_dev = torch.from_numpy(s).to(dev), torch.from_numpy(d).to(dev)
+    off, verts, ent = phg.trace_device(field, s_dev, d_dev, params)
+    lens = torch.diff(off)
+    off_r, verts_r, ent_r = phg.trace_device(field, s_dev.flip(0), d_dev.flip(0), params)
+    assert torch.equal(torch.diff(off_r).flip(0), lens)
+    assert torch.equal(ent_r.flip(0), ent)
+    assert int((lens - 1).sum()) == int(verts.shape[0]) - len(s)
+
+    pick = np.sort(np.random.Generator(np.random.Philox(key=77)).choice(len(s), 2000,
+                                                                        replace=False))
+    off_h, ent_h = off.cpu().numpy(), ent.cpu().numpy()
+    offr_h = off_r.cpu().numpy()
+    vol = SimpleNamespace(origin=np.zeros(3), voxel_size=synth.VOXEL_MM, dims=occ.shape,
+                          occ=occ.cpu().numpy(), ori=ori.cpu().numpy())
+    slab, keep, ent_o = oracle_c.trace(vol.origin, vol.voxel_size, vol.occ, vol.ori, s[pick],
+                                       d[pick], params)
+    off_o, v_o = oracle_c.to_csr(slab, keep)
+    n = len(s)
+    for k, i in enumerate(pick):
+        got = verts[off_h[i]:off_h[i + 1]].cpu().numpy()
+        assert np.array_equal(got, v_o[off_o[k]:off_o[k + 1]]), i
+        assert bool(ent_h[i]) == bool(ent_o[k])
+        j = n - 1 - i  # position of seed i in the reversed launch
+        assert np.array_equal(got, verts_r[offr_h[j]:offr_h[j + 1]].cpu().numpy())
+
+
+def test_c5_full_size_properties(gpu, oracle_c):
+    """BASELINE C5 at full field size (1024^3, 10% fill; 1M seeds: half disk, half interior
+    traced both ways), device-resident: order independence of all lengths, and a random
+    sample of 1000 strands bit-exact against the oracle on the host copy of the field."""
+    from paper_2604_05794_b200 import phg, synth
+    from paper_2604_05794_b200.volume import DeviceField
+
+    torch = gpu.torch
+    dev = torch.device("cuda", 0)
+    cfg = synth.CONFIGS["C5"]
+    ori, occ = synth.make_field(cfg.kind, cfg.n, dev)
+    field = DeviceField(np.zeros(3), synth.VOXEL_MM, occ, ori,
+                        torch.cuda.current_stream(dev).cuda_stream)
+    s, d = synth.config_seeds(cfg, 1_000_000, ori, occ)
+    params = phg.PhgParams(field_seeds=0, batch_size=len(s))
+    s_dev, d_dev = torch.from_numpy(s).to(dev), torch.from_numpy(d).to(dev)
+    off, verts, ent = phg.trace_device(field, s_dev, d_dev, params)
+    lens = torch.diff(off)
+    assert int(lens.max()) > 4 * float(lens.float().median())  # divergent lengths
+    off_r, _, ent_r = phg.trace_device(field, s_dev.flip(0), d_dev.flip(0), params)
+    assert torch.equal(torch.diff(off_r).flip(0), lens)
+    assert torch.equal(ent_r.flip(0), ent)
+
+    pick = np.sort(np.random.Generator(np.random.Philox(key=78)).choice(len(s), 1000,
+                                                                        replace=False))
+    off_h, ent_h = off.cpu().numpy(), ent.cpu().numpy()
+    occ_h, ori_h = occ.cpu().numpy(), ori.cpu().numpy()
+    del ori, occ
+    slab, keep, ent_o = oracle_c.trace(np.zeros(3), synth.VOXEL_MM, occ_h, ori_h, s[pick],
+                                       d[pick], params)
+    off_o, v_o = oracle_c.to_csr(slab, keep)
+    for k, i in enumerate(pick):
+        got = verts[off_h[i]:off_h[i + 1]].cpu().numpy()
+        assert np.array_equal(got, v_o[off_o[k]:off_o[k + 1]]), i
+        assert bool(ent_h[i]) == bool(ent_o[k])
