@@ -46,8 +46,8 @@ def parse():
     ap.add_argument("--cpu-sample", type=int, default=0, help="seeds in the CPU sample")
     ap.add_argument("--sweep", action="store_true", help="time every trace-kernel variant")
     ap.add_argument("--no-driver", action="store_true", help="skip the batch-driver leg")
-    ap.add_argument("--sweep-sizes", action="store_true",
-                    help="one-lane vs 8-lane trace kernel across launch sizes")
+    ap.add_argument("--sweep-sizes", default=None, metavar="V,V,...",
+                    help="time the given trace-kernel variants across launch sizes")
     ap.add_argument("--e2e-chunk", type=int, default=0,
                     help="seeds per chunk of the pipelined host path (0: library default)")
     return ap.parse_args()
@@ -292,7 +292,7 @@ def run_ours(args):
         return
     if args.sweep_sizes:
         sweep_launch_sizes(field, s_dev, d_dev, params, tracer, stream,
-                           list(range(min(2, _native_variants()))))
+                           [int(v) for v in args.sweep_sizes.split(",")])
         return
 
     for _ in range(args.warmup):
