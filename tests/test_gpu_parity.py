@@ -266,6 +266,42 @@ def test_errors_map_to_reference_types(gpu):
     assert gpu.phg.trace_batch(vol, np.zeros((0, 3)), np.zeros((0, 3)), P()) == []
 
 
+def test_field_with_border_beyond_32bit_index_is_rejected(gpu):
+    """The padded field ((nx+2)(ny+2)(nz+2) voxels) must index in 32 bits: 1626^3 fits
+    unpadded but not with its border; the check runs before any array is read."""
+    import ctypes
+
+    from paper_2604_05794_b200 import _native
+
+    lib = _native.load()
+    f = ctypes.c_void_p()
+    tiny = np.zeros(3, np.float32)
+    org = np.zeros(3)
+    rc = lib.phg_field_create(ctypes.byref(f), tiny.ctypes.data, tiny.ctypes.data, 1626, 1626,
+                              1626, org.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                              ctypes.c_double(2.0), None)
+    assert rc == _native.PHG_ERR_INVALID and not f.value
+    assert b"border" in lib.phg_last_error()
+
+
+@pytest.mark.parametrize("dims", [(1, 1, 40), (2, 1, 3), (1, 7, 1), (3, 3, 3)])
+def test_degenerate_dims_bit_exact(gpu, oracle_c, dims):
+    """Fields one or two voxels thick on some axis (every corner block touches the border)."""
+    rng = np.random.Generator(np.random.Philox(key=sum(dims)))
+    occ = rng.random(dims) < 0.7
+    ori = rng.normal(size=dims + (3,)).astype(np.float32)
+    ori[..., 2] = np.abs(ori[..., 2]) + 0.5
+    vol = SimpleNamespace(origin=np.array([-0.3, 0.2, 0.1]), voxel_size=2.0, dims=dims, occ=occ,
+                          ori=ori)
+    ext = np.array(dims) * 2.0
+    s = vol.origin + rng.random((300, 3)) * ext * 1.2 - 0.1 * ext
+    d = rng.normal(size=(300, 3))
+    p = SimpleNamespace(step_mm=0.7, max_vertices=60, min_support=0.05, probe_steps=4,
+                        coast_steps=3, steer=0.0, strict=False)
+    _compare_with_oracle(gpu, oracle_c, vol, s, d, p)
+    assert gpu.phg._tracer().last_sampler() == "fast-pow2"
+
+
 def test_install_reroutes_module_global(gpu):
     """install() replaces trace_batch on a reference-shaped module and disables the fork pool."""
     import types
