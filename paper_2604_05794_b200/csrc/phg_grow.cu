@@ -330,6 +330,76 @@ void swap_buf(DevBuf& a, DevBuf& b) {
     std::swap(a.cap, b.cap);
 }
 
+// ---- speculative deferred-commit batches ------------------------------------------------------
+// Every batch of a phase is traced in ONE launch against the cap plane P0 at the start of the
+// phase; batch b must see the plane P_b after batches < b committed (phg.py:236).  Counts only
+// grow (a uint16 wrap ends the speculation), so P0 is a subset of P_b, and a cap probe
+// differs between the two planes only where P_b holds a voxel P0 did not -- there the strand
+// dies instead of continuing (phg.py:140-142).  Up to its first such probe the strand is the
+// same under both planes, so its exact trace under P_b is the speculative one truncated there.
+//
+// A probe is a step that appends vertex t while entered (some step <= t was supported,
+// phg.py:127) into a voxel other than that of vertex t-1 (t = 1: always; phg.py:139, the
+// trace kernel's new_vox).  Truncating at t keeps vertices [0, t) and, the strand being
+// entered, keep = max(last supported step <= t, 1) of them (phg.py:124, :158).  The trace kernel
+// records which appended steps were supported (TraceRecord); vertex cells are recomputed from
+// the slab with the kernel's own arithmetic.  One warp per strand, 32 vertices per pass.
+__global__ void spec_truncate_kernel(FieldView F, const double* __restrict__ slab, size_t rs,
+                                     const uint32_t* __restrict__ bits, int words,
+                                     const int32_t* __restrict__ nverts, long long n,
+                                     long long* __restrict__ keep) {
+    const int lane = threadIdx.x & 31;
+    const long long warp = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+    const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+    for (long long i = warp; i < n; i += nwarps) {
+        const int m = nverts[i];
+        const double* row = slab + (size_t)i * rs;
+        const uint32_t* b = bits + (size_t)i * words;
+        // bit t (1 <= t < m) of the words: step t was supported; the first one enters
+        int first_sup = INT_MAX;
+        for (int w = 0; 32 * w < m && first_sup == INT_MAX; ++w) {
+            uint32_t x = b[w];
+            if (w == 0) x &= ~1u;
+            const int valid = m - 32 * w;
+            if (valid < 32) x &= (1u << valid) - 1u;
+            if (x) first_sup = 32 * w + __ffs(x) - 1;
+        }
+        if (first_sup == INT_MAX) continue;  // never entered: no cap probes at all
+        int cut = -1;
+        uint32_t carry = 0xffffffffu;  // cell of the last vertex of the previous pass
+        for (int base = 0; base < m && cut < 0; base += 32) {
+            const int t = base + lane;
+            const bool step = t >= 1 && t < m;
+            uint32_t lin = 0xffffffffu;
+            if (step) {
+                const int vx = floor_sat(grid_coord(F, row[3 * t + 0] - F.ox));
+                const int vy = floor_sat(grid_coord(F, row[3 * t + 1] - F.oy));
+                const int vz = floor_sat(grid_coord(F, row[3 * t + 2] - F.oz));
+                lin = ((uint32_t)vx * F.ny + vy) * F.nz + vz;
+            }
+            uint32_t prev = __shfl_up_sync(kFull, lin, 1);
+            if (lane == 0) prev = carry;
+            const bool probe = step && t >= first_sup && (t == 1 || lin != prev) &&
+                               ((__ldg(F.cap + (lin >> 5)) >> (lin & 31)) & 1u);
+            const unsigned hit = __ballot_sync(kFull, probe);
+            if (hit) cut = base + __ffs(hit) - 1;
+            carry = __shfl_sync(kFull, lin, 31);
+        }
+        if (cut < 0 || lane != 0) continue;
+        int last = 1;  // strand_init's last_sup
+        for (int w = cut >> 5; w >= 0; --w) {
+            uint32_t x = b[w];
+            if (w == 0) x &= ~1u;
+            if (w == (cut >> 5) && (cut & 31) != 31) x &= (2u << (cut & 31)) - 1u;
+            if (x) {
+                last = 32 * w + 31 - __clz(x);
+                break;
+            }
+        }
+        keep[i] = last > 1 ? last : 1;
+    }
+}
+
 // grow `b` to hold `need` bytes keeping its first `used` bytes
 phg_status grow_keep(DevBuf& b, size_t used, size_t need, cudaStream_t st) {
     if (need <= b.cap) return PHG_OK;
@@ -484,6 +554,37 @@ phg_status batch_scratch(GrowCtx& G, long long n, BatchScratch& B) {
     return PHG_OK;
 }
 
+// segments, commits and output of one traced batch of scalp seeds (phg.py:242-251)
+phg_status scalp_post(GrowCtx& G, const double* slab, const long long* keep, const uint8_t* ent,
+                      long long nb, bool export_commits, long long* segs_added) {
+    GrowSession& S = *G.s;
+    phg_ctx* c = G.c;
+    BatchScratch B;
+    PHG_TRY(batch_scratch(G, nb, B));
+    segment_select_kernel<<<grid_for(nb, 256), 256, 0, G.st>>>(
+        keep, ent, nb, B.lens, B.segf, B.valid, S.misc.as<unsigned long long>());
+    PHG_CUDA(cudaGetLastError());
+    // direct commits go before the synchronising offsets step, which also picks up a uint16
+    // wrap flag they may raise; exported commits need the batch size to size their list
+    if (!export_commits)
+        PHG_TRY(commit_batch(G, slab, keep, nullptr, nullptr, B.valid, nb, 0, false));
+    long long nv = 0, ns = 0;
+    PHG_TRY(batch_offsets(G, nb, B.lens, B.segf, B.voff, B.sidx, &nv, &ns));
+    if (export_commits)
+        PHG_TRY(commit_batch(G, slab, keep, nullptr, nullptr, B.valid, nb, nv, true));
+    PHG_TRY(ensure_output(G, ns, nv));
+    gather_scalp_kernel<<<grid_for(nb * 32, 256, num_sms() * 16), 256, 0, G.st>>>(
+        slab, row_stride_doubles(S.p.max_vertices), keep, B.valid, B.voff, B.sidx, nb, S.verts,
+        S.segs, c->g_out_off.as<long long>(), c->g_out_verts.as<double>(),
+        c->g_out_rooted.as<uint8_t>());
+    PHG_CUDA(cudaGetLastError());
+    S.segs += ns;
+    S.verts += nv;
+    S.scalp_segs = S.segs;
+    *segs_added = ns;
+    return PHG_OK;
+}
+
 // one deferred-commit batch of scalp seeds (phg.py:229-251)
 phg_status scalp_batch(GrowCtx& G, const double* d_pos, const double* d_dir, long long nb,
                        bool export_commits, long long* segs_added) {
@@ -494,33 +595,8 @@ phg_status scalp_batch(GrowCtx& G, const double* d_pos, const double* d_dir, lon
     if (nb == 0) return PHG_OK;
     PHG_TRY(set_cap_plane(G));
     PHG_TRY(trace_core(c, S.f, &S.p, d_pos, d_dir, nb, S.strict ? S.counts : nullptr, G.st));
-    BatchScratch B;
-    PHG_TRY(batch_scratch(G, nb, B));
-    const long long* keep = c->keep.as<long long>();
-    segment_select_kernel<<<grid_for(nb, 256), 256, 0, G.st>>>(
-        keep, c->entered.as<uint8_t>(), nb, B.lens, B.segf, B.valid, S.misc.as<unsigned long long>());
-    PHG_CUDA(cudaGetLastError());
-    // direct commits go before the synchronising offsets step, which also picks up a uint16
-    // wrap flag they may raise; exported commits need the batch size to size their list
-    if (!export_commits)
-        PHG_TRY(commit_batch(G, c->slab.as<double>(), keep, nullptr, nullptr, B.valid, nb, 0,
-                             false));
-    long long nv = 0, ns = 0;
-    PHG_TRY(batch_offsets(G, nb, B.lens, B.segf, B.voff, B.sidx, &nv, &ns));
-    if (export_commits)
-        PHG_TRY(commit_batch(G, c->slab.as<double>(), keep, nullptr, nullptr, B.valid, nb, nv,
-                             true));
-    PHG_TRY(ensure_output(G, ns, nv));
-    gather_scalp_kernel<<<grid_for(nb * 32, 256, num_sms() * 16), 256, 0, G.st>>>(
-        c->slab.as<double>(), row_stride_doubles(S.p.max_vertices), keep, B.valid, B.voff, B.sidx,
-        nb, S.verts, S.segs, c->g_out_off.as<long long>(), c->g_out_verts.as<double>(),
-        c->g_out_rooted.as<uint8_t>());
-    PHG_CUDA(cudaGetLastError());
-    S.segs += ns;
-    S.verts += nv;
-    S.scalp_segs = S.segs;
-    *segs_added = ns;
-    return PHG_OK;
+    return scalp_post(G, c->slab.as<double>(), c->keep.as<long long>(), c->entered.as<uint8_t>(),
+                      nb, export_commits, segs_added);
 }
 
 // field seeds (phg.py:266-275): unvisited occupied voxels, strided, centres + unit ori
@@ -586,6 +662,38 @@ phg_status field_begin(GrowCtx& G) {
     return PHG_OK;
 }
 
+// joins, commits and output of one traced batch of field seeds (phg.py:294-302); rows of the
+// forward traces in slab_f/keep_f/ent_f, of the backward ones in slab_b/keep_b/ent_b
+phg_status field_post(GrowCtx& G, const double* slab_f, const long long* keep_f,
+                      const uint8_t* ent_f, const double* slab_b, const long long* keep_b,
+                      const uint8_t* ent_b, long long nb, bool export_commits,
+                      long long* segs_added) {
+    GrowSession& S = *G.s;
+    phg_ctx* c = G.c;
+    const size_t rs = row_stride_doubles(S.p.max_vertices);
+    BatchScratch B;
+    PHG_TRY(batch_scratch(G, nb, B));
+    join_select_kernel<<<grid_for(nb, 256), 256, 0, G.st>>>(keep_f, ent_f, keep_b, ent_b, nb,
+                                                            B.lens, B.segf, B.valid);
+    PHG_CUDA(cudaGetLastError());
+    if (!export_commits)
+        PHG_TRY(commit_batch(G, slab_f, keep_f, slab_b, keep_b, B.valid, nb, 0, false));
+    long long nv = 0, ns = 0;
+    PHG_TRY(batch_offsets(G, nb, B.lens, B.segf, B.voff, B.sidx, &nv, &ns));
+    // a joined segment's voxels are those of its two traces: at most L + 1 distinct ids
+    if (export_commits)
+        PHG_TRY(commit_batch(G, slab_f, keep_f, slab_b, keep_b, B.valid, nb, nv + ns, true));
+    PHG_TRY(ensure_output(G, ns, nv));
+    gather_joined_kernel<<<grid_for(nb * 32, 256, num_sms() * 16), 256, 0, G.st>>>(
+        slab_f, slab_b, rs, keep_f, keep_b, B.valid, B.voff, B.sidx, nb, S.verts, S.segs,
+        c->g_out_off.as<long long>(), c->g_out_verts.as<double>(), c->g_out_rooted.as<uint8_t>());
+    PHG_CUDA(cudaGetLastError());
+    S.segs += ns;
+    S.verts += nv;
+    *segs_added = ns;
+    return PHG_OK;
+}
+
 // one batch of field seeds [first, first + nb): trace +d and -d against the same frozen plane,
 // join, keep, commit (phg.py:277-302)
 phg_status field_batch(GrowCtx& G, long long first, long long nb, bool export_commits,
@@ -640,26 +748,108 @@ phg_status field_batch(GrowCtx& G, long long first, long long nb, bool export_co
         keep_b = c->keep.as<long long>();
         ent_b = c->entered.as<uint8_t>();
     }
-    BatchScratch B;
-    PHG_TRY(batch_scratch(G, nb, B));
-    join_select_kernel<<<grid_for(nb, 256), 256, 0, G.st>>>(keep_f, ent_f, keep_b, ent_b, nb,
-                                                            B.lens, B.segf, B.valid);
+    return field_post(G, slab_f, keep_f, ent_f, slab_b, keep_b, ent_b, nb, export_commits,
+                      segs_added);
+}
+
+// ---- speculative phases of phg_grow_init (see spec_truncate_kernel) ---------------------------
+phg_status rec_buffers(GrowCtx& G, long long n, TraceRecord& R) {
+    const int words = (G.s->p.max_vertices + 31) / 32;
+    PHG_TRY(G.c->g_rec_bits.ensure((size_t)n * words * 4));
+    PHG_TRY(G.c->g_rec_nv.ensure((size_t)n * 4));
+    R = TraceRecord{G.c->g_rec_bits.as<uint32_t>(), G.c->g_rec_nv.as<int32_t>(), words};
+    return PHG_OK;
+}
+
+// exact trace of rows [first, first + nb) under the current plane: truncate in place (keep)
+phg_status spec_truncate(GrowCtx& G, const TraceRecord& R, long long first, long long nb) {
+    GrowSession& S = *G.s;
+    const size_t rs = row_stride_doubles(S.p.max_vertices);
+    spec_truncate_kernel<<<grid_for(nb * 32, 256, num_sms() * 16), 256, 0, G.st>>>(
+        S.f->view(), G.c->slab.as<double>() + (size_t)first * rs, rs,
+        R.bits + (size_t)first * R.words, R.words, R.nverts + first, nb,
+        G.c->keep.as<long long>() + first);
     PHG_CUDA(cudaGetLastError());
-    if (!export_commits)
-        PHG_TRY(commit_batch(G, slab_f, keep_f, slab_b, keep_b, B.valid, nb, 0, false));
-    long long nv = 0, ns = 0;
-    PHG_TRY(batch_offsets(G, nb, B.lens, B.segf, B.voff, B.sidx, &nv, &ns));
-    // a joined segment's voxels are those of its two traces: at most L + 1 distinct ids
-    if (export_commits)
-        PHG_TRY(commit_batch(G, slab_f, keep_f, slab_b, keep_b, B.valid, nb, nv + ns, true));
-    PHG_TRY(ensure_output(G, ns, nv));
-    gather_joined_kernel<<<grid_for(nb * 32, 256, num_sms() * 16), 256, 0, G.st>>>(
-        slab_f, slab_b, rs, keep_f, keep_b, B.valid, B.voff, B.sidx, nb, S.verts, S.segs,
-        c->g_out_off.as<long long>(), c->g_out_verts.as<double>(), c->g_out_rooted.as<uint8_t>());
+    return PHG_OK;
+}
+
+// PHG_DRIVER_SPEC=0 turns the speculation off (per-batch traces, for comparison)
+bool spec_enabled() {
+    const char* e = getenv("PHG_DRIVER_SPEC");
+    return !(e && e[0] == '0');
+}
+
+// every scalp batch (phg.py:229-251): one trace against the plane at the start, then per
+// batch in order: truncate to the current plane, select, commit, emit.  After a uint16 wrap
+// the plane is no longer a superset of the start plane: the remaining batches trace afresh.
+phg_status scalp_phase_spec(GrowCtx& G, const double* pos, const double* dir, long long n) {
+    GrowSession& S = *G.s;
+    phg_ctx* c = G.c;
+    const long long bs = S.g.batch_size;
+    const size_t rs = row_stride_doubles(S.p.max_vertices);
+    PHG_TRY(set_cap_plane(G));
+    TraceRecord R;
+    PHG_TRY(rec_buffers(G, n, R));
+    PHG_TRY(trace_core(c, S.f, &S.p, pos, dir, n, nullptr, G.st, &R));
+    long long added = 0;
+    for (long long b0 = 0; b0 < n; b0 += bs) {
+        const long long nb = std::min(bs, n - b0);
+        if (!S.cap_valid) {
+            for (long long r0 = b0; r0 < n; r0 += bs)
+                PHG_TRY(scalp_batch(G, pos + 3 * r0, dir + 3 * r0, std::min(bs, n - r0), false,
+                                    &added));
+            return PHG_OK;
+        }
+        if (b0 > 0) PHG_TRY(spec_truncate(G, R, b0, nb));  // batch 0 saw the start plane
+        PHG_TRY(scalp_post(G, c->slab.as<double>() + (size_t)b0 * rs,
+                           c->keep.as<long long>() + b0, c->entered.as<uint8_t>() + b0, nb, false,
+                           &added));
+    }
+    return PHG_OK;
+}
+
+// every field batch (phg.py:277-302) the same way: one launch of all +d rows [0, nf) and -d
+// rows [nf, 2nf) against the plane after the scalp phase
+phg_status field_phase_spec(GrowCtx& G) {
+    GrowSession& S = *G.s;
+    phg_ctx* c = G.c;
+    const long long nf = S.nf_seeds, bs = S.g.batch_size;
+    if (nf == 0) return PHG_OK;
+    const size_t rs = row_stride_doubles(S.p.max_vertices);
+    PHG_TRY(set_cap_plane(G));
+    const double* pos = c->g_fpos.as<double>();
+    const double* dir = c->g_fdir.as<double>();
+    PHG_TRY(c->g_neg_dir.ensure((size_t)nf * 24 * 4));
+    double* pos2 = c->g_neg_dir.as<double>();
+    double* dir2 = pos2 + 6 * nf;
+    PHG_CUDA(cudaMemcpyAsync(pos2, pos, (size_t)nf * 24, cudaMemcpyDeviceToDevice, G.st));
+    PHG_CUDA(cudaMemcpyAsync(pos2 + 3 * nf, pos, (size_t)nf * 24, cudaMemcpyDeviceToDevice, G.st));
+    PHG_CUDA(cudaMemcpyAsync(dir2, dir, (size_t)nf * 24, cudaMemcpyDeviceToDevice, G.st));
+    negate_kernel<<<grid_for(nf * 3, 256, num_sms() * 16), 256, 0, G.st>>>(dir, dir2 + 3 * nf,
+                                                                            nf * 3);
     PHG_CUDA(cudaGetLastError());
-    S.segs += ns;
-    S.verts += nv;
-    *segs_added = ns;
+    TraceRecord R;
+    PHG_TRY(rec_buffers(G, 2 * nf, R));
+    PHG_TRY(trace_core(c, S.f, &S.p, pos2, dir2, 2 * nf, nullptr, G.st, &R));
+    long long added = 0;
+    const double* slab = c->slab.as<double>();
+    const long long* keep = c->keep.as<long long>();
+    const uint8_t* ent = c->entered.as<uint8_t>();
+    for (long long b0 = 0; b0 < nf; b0 += bs) {
+        const long long nb = std::min(bs, nf - b0);
+        if (!S.cap_valid) {
+            for (long long r0 = b0; r0 < nf; r0 += bs)
+                PHG_TRY(field_batch(G, r0, std::min(bs, nf - r0), false, &added));
+            return PHG_OK;
+        }
+        if (b0 > 0) {
+            PHG_TRY(spec_truncate(G, R, b0, nb));
+            PHG_TRY(spec_truncate(G, R, nf + b0, nb));
+        }
+        PHG_TRY(field_post(G, slab + (size_t)b0 * rs, keep + b0, ent + b0,
+                           slab + (size_t)(nf + b0) * rs, keep + nf + b0, ent + nf + b0, nb,
+                           false, &added));
+    }
     return PHG_OK;
 }
 
@@ -844,13 +1034,22 @@ phg_status phg_grow_init(phg_ctx* c, phg_field* f, const phg_params_v1* p,
     phg_status s = PHG_OK;
     const long long bs = g->batch_size;
     long long added = 0;
-    for (long long b0 = 0; s == PHG_OK && b0 < n; b0 += bs)
-        s = scalp_batch(G, (const double*)d_pos + 3 * b0, (const double*)d_dir + 3 * b0,
-                        std::min(bs, n - b0), false, &added);
+    const bool spec = !G.s->strict && spec_enabled();
+    if (spec && n > 0) {
+        s = scalp_phase_spec(G, (const double*)d_pos, (const double*)d_dir, n);
+    } else {
+        for (long long b0 = 0; s == PHG_OK && b0 < n; b0 += bs)
+            s = scalp_batch(G, (const double*)d_pos + 3 * b0, (const double*)d_dir + 3 * b0,
+                            std::min(bs, n - b0), false, &added);
+    }
     if (s == PHG_OK && n > 0 && g->field_seeds > 0) {
         s = field_begin(G);
-        for (long long b0 = 0; s == PHG_OK && b0 < G.s->nf_seeds; b0 += bs)
-            s = field_batch(G, b0, std::min(bs, G.s->nf_seeds - b0), false, &added);
+        if (s == PHG_OK && spec) {
+            s = field_phase_spec(G);
+        } else {
+            for (long long b0 = 0; s == PHG_OK && b0 < G.s->nf_seeds; b0 += bs)
+                s = field_batch(G, b0, std::min(bs, G.s->nf_seeds - b0), false, &added);
+        }
     }
     if (s != PHG_OK) {
         f->has_cap = false;

@@ -176,3 +176,34 @@ def test_device_driver_matches_oracle_at_scale(oracle_c):
     assert np.array_equal(off, off_o) and np.array_equal(rooted, rooted_o)
     assert np.array_equal(verts, verts_o)
     assert rep["n_scalp_segments"] > 1000 and rep["n_segments"] > rep["n_scalp_segments"]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cap,kind", [(1, "curly"), (2, "sparse"), (16, "wavy")])
+def test_speculative_driver_equals_sequential(monkeypatch, cap, kind):
+    """phg_grow_init traces all batches of a phase in one launch against the plane at the start
+    and truncates each batch to the plane it must see (csrc/phg_grow.cu, spec_truncate_kernel).
+    With 24 batches and a low cap most later strands are cut; the result must equal the
+    per-batch traces (PHG_DRIVER_SPEC=0) in segments, order and counts."""
+    from paper_2604_05794_b200 import grow, synth
+    from paper_2604_05794_b200.volume import OOVolume
+
+    ori, occ = synth.make_field(kind, 96, "cpu")
+    ori, occ = ori.numpy(), occ.numpy()
+    seeds, dirs = synth.disk_seeds(96, 24_000, 61, radius_frac=0.45)
+    params = _params(dict(batch_size=1000, occupancy_cap=cap, field_seeds=6000, max_vertices=250))
+
+    def run(spec):
+        monkeypatch.setenv("PHG_DRIVER_SPEC", "1" if spec else "0")
+        vol = OOVolume.empty((0, 0, 0), synth.VOXEL_MM, occ.shape)
+        vol.occ, vol.ori = occ, ori
+        segs, rep = grow.init_guide_strands(SimpleNamespace(seeds=seeds, seed_normals=dirs), vol,
+                                            params)
+        return _csr([(s.vertices, s.rooted) for s in segs]), vol.counts.copy(), rep
+
+    (off_s, v_s, r_s), counts_s, rep_s = run(True)
+    (off_q, v_q, r_q), counts_q, rep_q = run(False)
+    assert rep_s == rep_q and rep_s["n_segments"] > 0
+    assert np.array_equal(off_s, off_q) and np.array_equal(r_s, r_q)
+    assert np.array_equal(v_s, v_q)
+    assert np.array_equal(counts_s, counts_q)
