@@ -782,28 +782,46 @@ bool spec_enabled() {
 // every scalp batch (phg.py:229-251): one trace against the plane at the start, then per
 // batch in order: truncate to the current plane, select, commit, emit.  After a uint16 wrap
 // the plane is no longer a superset of the start plane: the remaining batches trace afresh.
+// Seeds per speculative launch: whole batches, about four times the trace kernel's resident
+// lanes (16 batches of the reference's 16384 on a B200).  One launch for the whole phase
+// traces every strand to full length against an empty plane; windows re-freeze the plane, so
+// later launches stop at the caps earlier batches filled (measured on 1M C3 seeds: 30.8 ms
+// for one launch, 22.1 ms for 16-batch windows, 29.7 ms for 4).  PHG_SPEC_WINDOW=<batches>
+// overrides.
+long long spec_window(long long bs) {
+    const char* e = getenv("PHG_SPEC_WINDOW");
+    long long w = (e && *e) ? atoll(e) : 0;
+    if (w <= 0) w = std::max(1ll, (4ll * num_sms() * 4 * kTPB + bs / 2) / bs);
+    return w * bs;
+}
+
 phg_status scalp_phase_spec(GrowCtx& G, const double* pos, const double* dir, long long n) {
     GrowSession& S = *G.s;
     phg_ctx* c = G.c;
     const long long bs = S.g.batch_size;
     const size_t rs = row_stride_doubles(S.p.max_vertices);
-    PHG_TRY(set_cap_plane(G));
-    TraceRecord R;
-    PHG_TRY(rec_buffers(G, n, R));
-    PHG_TRY(trace_core(c, S.f, &S.p, pos, dir, n, nullptr, G.st, &R));
+    const long long win = spec_window(bs);
     long long added = 0;
-    for (long long b0 = 0; b0 < n; b0 += bs) {
-        const long long nb = std::min(bs, n - b0);
-        if (!S.cap_valid) {
-            for (long long r0 = b0; r0 < n; r0 += bs)
-                PHG_TRY(scalp_batch(G, pos + 3 * r0, dir + 3 * r0, std::min(bs, n - r0), false,
-                                    &added));
-            return PHG_OK;
+    for (long long w0 = 0; w0 < n; w0 += win) {
+        const long long nw = std::min(win, n - w0);
+        PHG_TRY(set_cap_plane(G));
+        TraceRecord R;
+        PHG_TRY(rec_buffers(G, nw, R));
+        PHG_TRY(trace_core(c, S.f, &S.p, pos + 3 * w0, dir + 3 * w0, nw, nullptr, G.st, &R));
+        for (long long b0 = 0; b0 < nw; b0 += bs) {
+            const long long nb = std::min(bs, nw - b0);
+            if (!S.cap_valid) {  // a count wrapped: trace every remaining batch afresh
+                for (long long r0 = w0 + b0; r0 < n; r0 += bs)
+                    PHG_TRY(scalp_batch(G, pos + 3 * r0, dir + 3 * r0, std::min(bs, n - r0),
+                                        false, &added));
+                return PHG_OK;
+            }
+            if (b0 > 0) PHG_TRY(spec_truncate(G, R, b0, nb));  // the window's first batch saw
+                                                                // the plane it was traced with
+            PHG_TRY(scalp_post(G, c->slab.as<double>() + (size_t)b0 * rs,
+                               c->keep.as<long long>() + b0, c->entered.as<uint8_t>() + b0, nb,
+                               false, &added));
         }
-        if (b0 > 0) PHG_TRY(spec_truncate(G, R, b0, nb));  // batch 0 saw the start plane
-        PHG_TRY(scalp_post(G, c->slab.as<double>() + (size_t)b0 * rs,
-                           c->keep.as<long long>() + b0, c->entered.as<uint8_t>() + b0, nb, false,
-                           &added));
     }
     return PHG_OK;
 }

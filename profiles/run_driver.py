@@ -12,7 +12,7 @@ import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2604_05794_b200 import grow, synth  # noqa: E402
-from paper_2604_05794_b200.phg import PhgParams  # noqa: E402
+from paper_2604_05794_b200.phg import PhgParams, _tracer  # noqa: E402
 from paper_2604_05794_b200.volume import OOVolume  # noqa: E402
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 200_000
@@ -28,5 +28,6 @@ for r in range(reps):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     off, verts, rooted, rep = grow.init_guide_strands_csr(seeds, dirs, vol, PhgParams())
-    print(f"run {r}: {time.perf_counter() - t0:.3f} s  segments={len(rooted)} "
-          f"verts={len(verts)} {rep}", flush=True)
+    dev_ms = _tracer().last_kernel_ms()[1]
+    print(f"run {r}: {time.perf_counter() - t0:.3f} s  device {dev_ms:.2f} ms  "
+          f"segments={len(rooted)} verts={len(verts)} {rep}", flush=True)

@@ -179,12 +179,14 @@ def test_device_driver_matches_oracle_at_scale(oracle_c):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("cap,kind", [(1, "curly"), (2, "sparse"), (16, "wavy")])
-def test_speculative_driver_equals_sequential(monkeypatch, cap, kind):
+@pytest.mark.parametrize("cap,kind,window", [(1, "curly", "0"), (1, "curly", "5"),
+                                             (2, "sparse", "0"), (16, "wavy", "7")])
+def test_speculative_driver_equals_sequential(monkeypatch, cap, kind, window):
     """phg_grow_init traces all batches of a phase in one launch against the plane at the start
     and truncates each batch to the plane it must see (csrc/phg_grow.cu, spec_truncate_kernel).
     With 24 batches and a low cap most later strands are cut; the result must equal the
-    per-batch traces (PHG_DRIVER_SPEC=0) in segments, order and counts."""
+    per-batch traces (PHG_DRIVER_SPEC=0) in segments, order and counts.  ``window`` batches
+    per speculative launch (PHG_SPEC_WINDOW; 0 = the default, here the whole phase)."""
     from paper_2604_05794_b200 import grow, synth
     from paper_2604_05794_b200.volume import OOVolume
 
@@ -192,6 +194,8 @@ def test_speculative_driver_equals_sequential(monkeypatch, cap, kind):
     ori, occ = ori.numpy(), occ.numpy()
     seeds, dirs = synth.disk_seeds(96, 24_000, 61, radius_frac=0.45)
     params = _params(dict(batch_size=1000, occupancy_cap=cap, field_seeds=6000, max_vertices=250))
+
+    monkeypatch.setenv("PHG_SPEC_WINDOW", window)
 
     def run(spec):
         monkeypatch.setenv("PHG_DRIVER_SPEC", "1" if spec else "0")
