@@ -154,11 +154,9 @@ __global__ void apply_commits_kernel(const uint32_t* __restrict__ ids, long long
 // segment; for joined field segments the set spans both traces (voxels(bwd) U voxels(fwd)).
 // GLOBAL_TABLE: the per-warp table lives in global memory (very long segments).
 template <bool GLOBAL_TABLE>
-__global__ void commit_kernel(FieldView F, const double* __restrict__ slab_a,
-                              const long long* __restrict__ keep_a,
-                              const double* __restrict__ slab_b,
-                              const long long* __restrict__ keep_b,
-                              const uint8_t* __restrict__ valid, long long n, size_t row_stride,
+__global__ void commit_kernel(FieldView F, Rows slab_a, const long long* __restrict__ keep_a,
+                              Rows slab_b, const long long* __restrict__ keep_b,
+                              const uint8_t* __restrict__ valid, long long n,
                               CommitSink K, int bits, unsigned long long* __restrict__ gtables) {
     extern __shared__ unsigned long long smem_tables[];
     const int lane = threadIdx.x & 31;
@@ -173,15 +171,15 @@ __global__ void commit_kernel(FieldView F, const double* __restrict__ slab_a,
     for (long long i = gwarp; i < n; i += nwarps) {
         if (!valid[i]) continue;
         ++epoch;
-        commit_row(F, slab_a + (size_t)i * row_stride, keep_a[i], T, bits, epoch, K, lane);
-        if (slab_b) commit_row(F, slab_b + (size_t)i * row_stride, keep_b[i], T, bits, epoch, K,
+        commit_row(F, slab_a.row(i), keep_a[i], T, bits, epoch, K, lane);
+        if (slab_b.base) commit_row(F, slab_b.row(i), keep_b[i], T, bits, epoch, K,
                                lane);
         __syncwarp();
     }
 }
 
 // scalp segments -> output CSR (rows of valid strands, in seed order)
-__global__ void gather_scalp_kernel(const double* __restrict__ slab, size_t row_stride,
+__global__ void gather_scalp_kernel(Rows slab,
                                     const long long* __restrict__ keep,
                                     const uint8_t* __restrict__ valid,
                                     const long long* __restrict__ voff,
@@ -198,7 +196,7 @@ __global__ void gather_scalp_kernel(const double* __restrict__ slab, size_t row_
             out_off[sbase + sidx[i]] = o;
             rooted[sbase + sidx[i]] = 1;
         }
-        const double* src = slab + (size_t)i * row_stride;
+        const double* src = slab.row(i);
         double* dst = out_v + o * 3;
         const long long len = keep[i] * 3;
         for (long long j = lane; j < len; j += 32) dst[j] = src[j];
@@ -206,8 +204,7 @@ __global__ void gather_scalp_kernel(const double* __restrict__ slab, size_t row_
 }
 
 // field segments: v = concat(bwd[::-1], fwd[1:]) if len(bwd) > 1 else fwd (phg.py:294)
-__global__ void gather_joined_kernel(const double* __restrict__ slab_f,
-                                     const double* __restrict__ slab_b, size_t row_stride,
+__global__ void gather_joined_kernel(Rows slab_f, Rows slab_b,
                                      const long long* __restrict__ keep_f,
                                      const long long* __restrict__ keep_b,
                                      const uint8_t* __restrict__ valid,
@@ -226,8 +223,8 @@ __global__ void gather_joined_kernel(const double* __restrict__ slab_f,
             out_off[sbase + sidx[i]] = o;
             rooted[sbase + sidx[i]] = 0;
         }
-        const double* f = slab_f + (size_t)i * row_stride;
-        const double* b = slab_b + (size_t)i * row_stride;
+        const double* f = slab_f.row(i);
+        const double* b = slab_b.row(i);
         const long long lf = keep_f[i], lb = keep_b[i];
         double* dst = out_v + o * 3;
         if (lb > 1) {
@@ -344,7 +341,7 @@ void swap_buf(DevBuf& a, DevBuf& b) {
 // entered, keep = max(last supported step <= t, 1) of them (phg.py:124, :158).  The trace kernel
 // records which appended steps were supported (TraceRecord); vertex cells are recomputed from
 // the slab with the kernel's own arithmetic.  One warp per strand, 32 vertices per pass.
-__global__ void spec_truncate_kernel(FieldView F, const double* __restrict__ slab, size_t rs,
+__global__ void spec_truncate_kernel(FieldView F, Rows slab,
                                      const uint32_t* __restrict__ bits, int words,
                                      const int32_t* __restrict__ nverts, long long n,
                                      long long* __restrict__ keep) {
@@ -353,7 +350,7 @@ __global__ void spec_truncate_kernel(FieldView F, const double* __restrict__ sla
     const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
     for (long long i = warp; i < n; i += nwarps) {
         const int m = nverts[i];
-        const double* row = slab + (size_t)i * rs;
+        const double* row = slab.row(i);
         const uint32_t* b = bits + (size_t)i * words;
         // bit t (1 <= t < m) of the words: step t was supported; the first one enters
         int first_sup = INT_MAX;
@@ -456,13 +453,18 @@ CommitSink direct_sink(GrowSession& S) {
                       (unsigned int*)(S.misc.as<unsigned long long>() + 1), nullptr, nullptr};
 }
 
-phg_status launch_commit(GrowCtx& G, const double* slab_a, const long long* keep_a,
-                         const double* slab_b, const long long* keep_b, const uint8_t* valid,
+// rows of the last trace_core launch on the context
+Rows slab_rows(const GrowCtx& G) {
+    return Rows{G.c->slab.as<double>(), G.c->rows_by_queue ? G.c->rowmap.as<int32_t>() : nullptr,
+                row_stride_doubles(G.s->p.max_vertices)};
+}
+
+phg_status launch_commit(GrowCtx& G, Rows slab_a, const long long* keep_a, Rows slab_b,
+                         const long long* keep_b, const uint8_t* valid,
                          long long n, CommitSink K) {
     GrowSession& S = *G.s;
     const FieldView F = S.f->view();
-    const size_t rs = row_stride_doubles(S.p.max_vertices);
-    const long long max_entries = (long long)S.p.max_vertices * (slab_b ? 2 : 1);
+    const long long max_entries = (long long)S.p.max_vertices * (slab_b.base ? 2 : 1);
     int bits = 6;
     while ((1ll << bits) < 2 * max_entries) ++bits;
     const size_t table_bytes = (size_t)8 << bits;
@@ -474,11 +476,11 @@ phg_status launch_commit(GrowCtx& G, const double* slab_a, const long long* keep
         PHG_CUDA(cudaFuncSetAttribute(commit_kernel<false>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         commit_kernel<false><<<blocks, 32 * kCommitWarps, smem, G.st>>>(
-            F, slab_a, keep_a, slab_b, keep_b, valid, n, rs, K, bits, nullptr);
+            F, slab_a, keep_a, slab_b, keep_b, valid, n, K, bits, nullptr);
     } else {
         PHG_TRY(G.c->g_hash.ensure(table_bytes * (size_t)blocks * kCommitWarps));
         commit_kernel<true><<<blocks, 32 * kCommitWarps, 0, G.st>>>(
-            F, slab_a, keep_a, slab_b, keep_b, valid, n, rs, K, bits,
+            F, slab_a, keep_a, slab_b, keep_b, valid, n, K, bits,
             G.c->g_hash.as<unsigned long long>());
     }
     PHG_CUDA(cudaGetLastError());
@@ -486,8 +488,8 @@ phg_status launch_commit(GrowCtx& G, const double* slab_a, const long long* keep
 }
 
 // commit a batch: directly, or (export) into S.export_ids for an all-gather by the caller
-phg_status commit_batch(GrowCtx& G, const double* slab_a, const long long* keep_a,
-                        const double* slab_b, const long long* keep_b, const uint8_t* valid,
+phg_status commit_batch(GrowCtx& G, Rows slab_a, const long long* keep_a, Rows slab_b,
+                        const long long* keep_b, const uint8_t* valid,
                         long long n, long long max_ids, bool export_commits) {
     GrowSession& S = *G.s;
     S.n_export = 0;
@@ -555,7 +557,7 @@ phg_status batch_scratch(GrowCtx& G, long long n, BatchScratch& B) {
 }
 
 // segments, commits and output of one traced batch of scalp seeds (phg.py:242-251)
-phg_status scalp_post(GrowCtx& G, const double* slab, const long long* keep, const uint8_t* ent,
+phg_status scalp_post(GrowCtx& G, Rows slab, const long long* keep, const uint8_t* ent,
                       long long nb, bool export_commits, long long* segs_added) {
     GrowSession& S = *G.s;
     phg_ctx* c = G.c;
@@ -567,14 +569,14 @@ phg_status scalp_post(GrowCtx& G, const double* slab, const long long* keep, con
     // direct commits go before the synchronising offsets step, which also picks up a uint16
     // wrap flag they may raise; exported commits need the batch size to size their list
     if (!export_commits)
-        PHG_TRY(commit_batch(G, slab, keep, nullptr, nullptr, B.valid, nb, 0, false));
+        PHG_TRY(commit_batch(G, slab, keep, Rows{}, nullptr, B.valid, nb, 0, false));
     long long nv = 0, ns = 0;
     PHG_TRY(batch_offsets(G, nb, B.lens, B.segf, B.voff, B.sidx, &nv, &ns));
     if (export_commits)
-        PHG_TRY(commit_batch(G, slab, keep, nullptr, nullptr, B.valid, nb, nv, true));
+        PHG_TRY(commit_batch(G, slab, keep, Rows{}, nullptr, B.valid, nb, nv, true));
     PHG_TRY(ensure_output(G, ns, nv));
     gather_scalp_kernel<<<grid_for(nb * 32, 256, num_sms() * 16), 256, 0, G.st>>>(
-        slab, row_stride_doubles(S.p.max_vertices), keep, B.valid, B.voff, B.sidx, nb, S.verts,
+        slab, keep, B.valid, B.voff, B.sidx, nb, S.verts,
         S.segs, c->g_out_off.as<long long>(), c->g_out_verts.as<double>(),
         c->g_out_rooted.as<uint8_t>());
     PHG_CUDA(cudaGetLastError());
@@ -594,8 +596,9 @@ phg_status scalp_batch(GrowCtx& G, const double* d_pos, const double* d_dir, lon
     S.n_export = 0;
     if (nb == 0) return PHG_OK;
     PHG_TRY(set_cap_plane(G));
-    PHG_TRY(trace_core(c, S.f, &S.p, d_pos, d_dir, nb, S.strict ? S.counts : nullptr, G.st));
-    return scalp_post(G, c->slab.as<double>(), c->keep.as<long long>(), c->entered.as<uint8_t>(),
+    PHG_TRY(trace_core(c, S.f, &S.p, d_pos, d_dir, nb, S.strict ? S.counts : nullptr, G.st,
+                       nullptr, true));
+    return scalp_post(G, slab_rows(G), c->keep.as<long long>(), c->entered.as<uint8_t>(),
                       nb, export_commits, segs_added);
 }
 
@@ -664,13 +667,12 @@ phg_status field_begin(GrowCtx& G) {
 
 // joins, commits and output of one traced batch of field seeds (phg.py:294-302); rows of the
 // forward traces in slab_f/keep_f/ent_f, of the backward ones in slab_b/keep_b/ent_b
-phg_status field_post(GrowCtx& G, const double* slab_f, const long long* keep_f,
-                      const uint8_t* ent_f, const double* slab_b, const long long* keep_b,
+phg_status field_post(GrowCtx& G, Rows slab_f, const long long* keep_f,
+                      const uint8_t* ent_f, Rows slab_b, const long long* keep_b,
                       const uint8_t* ent_b, long long nb, bool export_commits,
                       long long* segs_added) {
     GrowSession& S = *G.s;
     phg_ctx* c = G.c;
-    const size_t rs = row_stride_doubles(S.p.max_vertices);
     BatchScratch B;
     PHG_TRY(batch_scratch(G, nb, B));
     join_select_kernel<<<grid_for(nb, 256), 256, 0, G.st>>>(keep_f, ent_f, keep_b, ent_b, nb,
@@ -685,7 +687,7 @@ phg_status field_post(GrowCtx& G, const double* slab_f, const long long* keep_f,
         PHG_TRY(commit_batch(G, slab_f, keep_f, slab_b, keep_b, B.valid, nb, nv + ns, true));
     PHG_TRY(ensure_output(G, ns, nv));
     gather_joined_kernel<<<grid_for(nb * 32, 256, num_sms() * 16), 256, 0, G.st>>>(
-        slab_f, slab_b, rs, keep_f, keep_b, B.valid, B.voff, B.sidx, nb, S.verts, S.segs,
+        slab_f, slab_b, keep_f, keep_b, B.valid, B.voff, B.sidx, nb, S.verts, S.segs,
         c->g_out_off.as<long long>(), c->g_out_verts.as<double>(), c->g_out_rooted.as<uint8_t>());
     PHG_CUDA(cudaGetLastError());
     S.segs += ns;
@@ -705,9 +707,8 @@ phg_status field_batch(GrowCtx& G, long long first, long long nb, bool export_co
     if (nb == 0) return PHG_OK;
     const double* pos = c->g_fpos.as<double>() + 3 * first;
     const double* dir = c->g_fdir.as<double>() + 3 * first;
-    const size_t rs = row_stride_doubles(S.p.max_vertices);
     PHG_TRY(set_cap_plane(G));
-    const double *slab_f, *slab_b;
+    Rows slab_f, slab_b;
     const long long *keep_f, *keep_b;
     const uint8_t *ent_f, *ent_b;
     if (!S.strict) {
@@ -723,9 +724,9 @@ phg_status field_batch(GrowCtx& G, long long first, long long nb, bool export_co
         negate_kernel<<<grid_for(nb * 3, 256, num_sms() * 16), 256, 0, G.st>>>(dir, dir2 + 3 * nb,
                                                                                 nb * 3);
         PHG_CUDA(cudaGetLastError());
-        PHG_TRY(trace_core(c, S.f, &S.p, pos2, dir2, 2 * nb, nullptr, G.st));
-        slab_f = c->slab.as<double>();
-        slab_b = slab_f + (size_t)nb * rs;
+        PHG_TRY(trace_core(c, S.f, &S.p, pos2, dir2, 2 * nb, nullptr, G.st, nullptr, true));
+        slab_f = slab_rows(G);
+        slab_b = slab_f.sub(nb);
         keep_f = c->keep.as<long long>();
         keep_b = keep_f + nb;
         ent_f = c->entered.as<uint8_t>();
@@ -741,10 +742,12 @@ phg_status field_batch(GrowCtx& G, long long first, long long nb, bool export_co
         negate_kernel<<<grid_for(nb * 3, 256, num_sms() * 16), 256, 0, G.st>>>(dir, ndir, nb * 3);
         PHG_CUDA(cudaGetLastError());
         PHG_TRY(trace_core(c, S.f, &S.p, pos, ndir, nb, S.counts, G.st));
-        slab_f = c->g_slab2.as<double>();
+        // (strict traces keep seed rows: no locality order)
+        const size_t rs = row_stride_doubles(S.p.max_vertices);
+        slab_f = Rows{c->g_slab2.as<double>(), nullptr, rs};
         keep_f = c->g_keep2.as<long long>();
         ent_f = c->g_ent2.as<uint8_t>();
-        slab_b = c->slab.as<double>();
+        slab_b = Rows{c->slab.as<double>(), nullptr, rs};
         keep_b = c->keep.as<long long>();
         ent_b = c->entered.as<uint8_t>();
     }
@@ -764,9 +767,8 @@ phg_status rec_buffers(GrowCtx& G, long long n, TraceRecord& R) {
 // exact trace of rows [first, first + nb) under the current plane: truncate in place (keep)
 phg_status spec_truncate(GrowCtx& G, const TraceRecord& R, long long first, long long nb) {
     GrowSession& S = *G.s;
-    const size_t rs = row_stride_doubles(S.p.max_vertices);
     spec_truncate_kernel<<<grid_for(nb * 32, 256, num_sms() * 16), 256, 0, G.st>>>(
-        S.f->view(), G.c->slab.as<double>() + (size_t)first * rs, rs,
+        S.f->view(), slab_rows(G).sub(first),
         R.bits + (size_t)first * R.words, R.words, R.nverts + first, nb,
         G.c->keep.as<long long>() + first);
     PHG_CUDA(cudaGetLastError());
@@ -799,7 +801,6 @@ phg_status scalp_phase_spec(GrowCtx& G, const double* pos, const double* dir, lo
     GrowSession& S = *G.s;
     phg_ctx* c = G.c;
     const long long bs = S.g.batch_size;
-    const size_t rs = row_stride_doubles(S.p.max_vertices);
     const long long win = spec_window(bs);
     long long added = 0;
     for (long long w0 = 0; w0 < n; w0 += win) {
@@ -807,7 +808,8 @@ phg_status scalp_phase_spec(GrowCtx& G, const double* pos, const double* dir, lo
         PHG_TRY(set_cap_plane(G));
         TraceRecord R;
         PHG_TRY(rec_buffers(G, nw, R));
-        PHG_TRY(trace_core(c, S.f, &S.p, pos + 3 * w0, dir + 3 * w0, nw, nullptr, G.st, &R));
+        PHG_TRY(trace_core(c, S.f, &S.p, pos + 3 * w0, dir + 3 * w0, nw, nullptr, G.st, &R,
+                           true));
         for (long long b0 = 0; b0 < nw; b0 += bs) {
             const long long nb = std::min(bs, nw - b0);
             if (!S.cap_valid) {  // a count wrapped: trace every remaining batch afresh
@@ -818,7 +820,7 @@ phg_status scalp_phase_spec(GrowCtx& G, const double* pos, const double* dir, lo
             }
             if (b0 > 0) PHG_TRY(spec_truncate(G, R, b0, nb));  // the window's first batch saw
                                                                 // the plane it was traced with
-            PHG_TRY(scalp_post(G, c->slab.as<double>() + (size_t)b0 * rs,
+            PHG_TRY(scalp_post(G, slab_rows(G).sub(b0),
                                c->keep.as<long long>() + b0, c->entered.as<uint8_t>() + b0, nb,
                                false, &added));
         }
@@ -833,7 +835,6 @@ phg_status field_phase_spec(GrowCtx& G) {
     phg_ctx* c = G.c;
     const long long nf = S.nf_seeds, bs = S.g.batch_size;
     if (nf == 0) return PHG_OK;
-    const size_t rs = row_stride_doubles(S.p.max_vertices);
     PHG_TRY(set_cap_plane(G));
     const double* pos = c->g_fpos.as<double>();
     const double* dir = c->g_fdir.as<double>();
@@ -848,9 +849,9 @@ phg_status field_phase_spec(GrowCtx& G) {
     PHG_CUDA(cudaGetLastError());
     TraceRecord R;
     PHG_TRY(rec_buffers(G, 2 * nf, R));
-    PHG_TRY(trace_core(c, S.f, &S.p, pos2, dir2, 2 * nf, nullptr, G.st, &R));
+    PHG_TRY(trace_core(c, S.f, &S.p, pos2, dir2, 2 * nf, nullptr, G.st, &R, true));
     long long added = 0;
-    const double* slab = c->slab.as<double>();
+    const Rows slab = slab_rows(G);
     const long long* keep = c->keep.as<long long>();
     const uint8_t* ent = c->entered.as<uint8_t>();
     for (long long b0 = 0; b0 < nf; b0 += bs) {
@@ -864,8 +865,8 @@ phg_status field_phase_spec(GrowCtx& G) {
             PHG_TRY(spec_truncate(G, R, b0, nb));
             PHG_TRY(spec_truncate(G, R, nf + b0, nb));
         }
-        PHG_TRY(field_post(G, slab + (size_t)b0 * rs, keep + b0, ent + b0,
-                           slab + (size_t)(nf + b0) * rs, keep + nf + b0, ent + nf + b0, nb,
+        PHG_TRY(field_post(G, slab.sub(b0), keep + b0, ent + b0,
+                           slab.sub(nf + b0), keep + nf + b0, ent + nf + b0, nb,
                            false, &added));
     }
     return PHG_OK;
