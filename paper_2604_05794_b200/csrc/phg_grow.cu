@@ -196,10 +196,7 @@ __global__ void gather_scalp_kernel(Rows slab,
             out_off[sbase + sidx[i]] = o;
             rooted[sbase + sidx[i]] = 1;
         }
-        const double* src = slab.row(i);
-        double* dst = out_v + o * 3;
-        const long long len = keep[i] * 3;
-        for (long long j = lane; j < len; j += 32) dst[j] = src[j];
+        copy_strand(slab.row(i), out_v + o * 3, keep[i] * 3, lane);
     }
 }
 
@@ -235,7 +232,7 @@ __global__ void gather_joined_kernel(Rows slab_f, Rows slab_b,
             dst += lb * 3;
             for (long long j = lane; j < (lf - 1) * 3; j += 32) dst[j] = f[3 + j];
         } else {
-            for (long long j = lane; j < lf * 3; j += 32) dst[j] = f[j];
+            copy_strand(f, dst, lf * 3, lane);
         }
     }
 }
