@@ -190,6 +190,48 @@ def test_sampler_forms_bit_exact(gpu, oracle_c, kind, vs, nan, want):
     assert gpu.phg._tracer().last_sampler() == want
 
 
+@pytest.mark.parametrize("case", ["orthogonal", "random-unit", "scaled-1e3", "scaled-1e-20"])
+@pytest.mark.parametrize("force_fp64", [False, True])
+def test_fp32_sign_fallback_bit_exact(gpu, oracle_c, case, force_fp64, monkeypatch):
+    """Fields and seeds on which the fp32 corner-sign certificate (Cfg::SIGN32) is unsure:
+    live corners exactly orthogonal to the query (d = +-0, incl. -0.0 components in ori and
+    seed directions), occupied voxels with ori 0, random unit ori (many near-orthogonal
+    corners), and ori far from unit length (the certificate scales with max|ori|).  Every
+    case must still equal the oracle bit for bit."""
+    n = 40
+    vol, s, d, p = _config_case("straight", n, 800, 41)
+    ori = vol.ori.copy()
+    rng = np.random.Generator(np.random.Philox(key=41))
+    if case == "orthogonal":
+        # horizontal seed directions on a vertical field: d = +-0 at every live corner
+        d = np.zeros_like(d)
+        k = rng.integers(0, 4, len(d))
+        d[k == 0] = (1.0, 0.0, 0.0)
+        d[k == 1] = (-1.0, -0.0, -0.0)
+        d[k == 2] = (0.0, -1.0, -0.0)
+        d[k == 3] = rng.normal(size=(int((k == 3).sum()), 3))
+        occ = vol.occ
+        holes = occ & (rng.random(occ.shape) < 0.05)
+        ori[holes] = 0.0                                   # occupied, ori exactly 0
+        negz = occ & (rng.random(occ.shape) < 0.2)
+        ori[negz] = np.array([-0.0, 0.0, 1.0], dtype=np.float32)  # -0.0 components
+    elif case == "random-unit":
+        r = rng.normal(size=ori.shape)
+        r /= np.linalg.norm(r, axis=-1, keepdims=True)
+        ori = np.where(vol.occ[..., None], r, 0.0).astype(np.float32)
+        d = rng.normal(size=d.shape)
+    else:
+        scale = 1e3 if case == "scaled-1e3" else 1e-20
+        tilt = rng.normal(scale=0.3, size=ori.shape).astype(np.float32)
+        ori = np.where(vol.occ[..., None], (ori + tilt) * np.float32(scale), 0.0)
+        ori = ori.astype(np.float32)
+    vol.ori = ori
+    if force_fp64:  # PHG_SIGN32=0: the fallback decides every sample's signs
+        monkeypatch.setenv("PHG_SIGN32", "0")
+    _compare_with_oracle(gpu, oracle_c, vol, s, d, p)
+    assert gpu.phg._tracer().last_sampler() == "fast-pow2"
+
+
 def synth_voxel():
     from paper_2604_05794_b200 import synth
 
