@@ -123,11 +123,25 @@ struct CommitSink {
 __device__ __forceinline__ void commit_row(const FieldView& F, const double* __restrict__ row,
                                            long long L, unsigned long long* T, int bits,
                                            uint32_t epoch, const CommitSink& K, int lane) {
+    // the next pass's vertex is loaded before this pass's hash insert and atomics, so the load
+    // latency overlaps them
+    double nx_ = 0.0, ny_ = 0.0, nz_ = 0.0;
+    if (lane < L) {
+        nx_ = row[3 * lane + 0];
+        ny_ = row[3 * lane + 1];
+        nz_ = row[3 * lane + 2];
+    }
     for (long long k = lane; k < L; k += 32) {
+        const double px = nx_, py = ny_, pz = nz_;
+        if (k + 32 < L) {
+            nx_ = row[3 * (k + 32) + 0];
+            ny_ = row[3 * (k + 32) + 1];
+            nz_ = row[3 * (k + 32) + 2];
+        }
         // vol.voxel_of (volume.py:42-45) and in_bounds (:47-49)
-        const int vx = floor_idx(grid_coord(F, row[3 * k + 0] - F.ox));
-        const int vy = floor_idx(grid_coord(F, row[3 * k + 1] - F.oy));
-        const int vz = floor_idx(grid_coord(F, row[3 * k + 2] - F.oz));
+        const int vx = floor_idx(grid_coord(F, px - F.ox));
+        const int vy = floor_idx(grid_coord(F, py - F.oy));
+        const int vz = floor_idx(grid_coord(F, pz - F.oz));
         if ((unsigned)vx < (unsigned)F.nx && (unsigned)vy < (unsigned)F.ny &&
             (unsigned)vz < (unsigned)F.nz) {
             const uint32_t lin = ((uint32_t)vx * F.ny + vy) * F.nz + vz;
@@ -465,10 +479,16 @@ phg_status launch_commit(GrowCtx& G, Rows slab_a, const long long* keep_a, Rows 
     int bits = 6;
     while ((1ll << bits) < 2 * max_entries) ++bits;
     const size_t table_bytes = (size_t)8 << bits;
-    const int warps_total = num_sms() * 16;
+    // as many warps as the per-warp tables let an SM hold (up to 32): each warp walks a few
+    // segments with a dependent load -> hash -> atomic chain, so warps in flight set the pace
+    const bool smem_tables = table_bytes * kCommitWarps <= 200 * 1024;
+    const int per_sm =
+        smem_tables ? (int)std::max<size_t>(kCommitWarps, std::min<size_t>(32, (200 * 1024) / table_bytes))
+                    : 16;
+    const int warps_total = num_sms() * per_sm;
     const int blocks = std::max(1, std::min(warps_total / kCommitWarps,
                                             (int)((n + kCommitWarps - 1) / kCommitWarps)));
-    if (table_bytes * kCommitWarps <= 200 * 1024) {
+    if (smem_tables) {
         const size_t smem = table_bytes * kCommitWarps;
         PHG_CUDA(cudaFuncSetAttribute(commit_kernel<false>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
