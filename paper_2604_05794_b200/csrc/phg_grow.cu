@@ -164,6 +164,36 @@ __global__ void apply_commits_kernel(const uint32_t* __restrict__ ids, long long
         bump_count(counts, cap_bits, cap, wrapped, ids[i]);
 }
 
+// undo exported commits (rollback of an optimistic window): counts[id] -= 1
+__global__ void uncommit_kernel(const uint32_t* __restrict__ ids, long long n,
+                                uint32_t* __restrict__ counts) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        atomicSub(counts + ids[i], 1u);
+}
+
+// sum of the appended vertex counts of a traced window (bounds its kept vertices)
+__global__ void sum_nverts_kernel(const int32_t* __restrict__ nv, long long n,
+                                  unsigned long long* __restrict__ out) {
+    unsigned long long acc = 0;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        acc += (unsigned long long)nv[i];
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(kFull, acc, o);
+    if ((threadIdx.x & 31) == 0 && acc) atomicAdd(out, acc);
+}
+
+// device output totals of asynchronous posts: dtot = {segments, vertices}
+__global__ void set_totals_kernel(long long* dtot, long long segs, long long verts) {
+    dtot[0] = segs;
+    dtot[1] = verts;
+}
+__global__ void advance_totals_kernel(long long* dtot, const long long* __restrict__ sidx_end,
+                                      const long long* __restrict__ voff_end) {
+    dtot[0] += *sidx_end;
+    dtot[1] += *voff_end;
+}
+
 // vol.counts[unique voxels of each valid segment] += 1 (phg.py:248-251, :299-302).  One warp per
 // segment; for joined field segments the set spans both traces (voxels(bwd) U voxels(fwd)).
 // GLOBAL_TABLE: the per-warp table lives in global memory (very long segments).
@@ -199,10 +229,15 @@ __global__ void gather_scalp_kernel(Rows slab,
                                     const long long* __restrict__ voff,
                                     const long long* __restrict__ sidx, long long n,
                                     long long vbase, long long sbase, long long* __restrict__ out_off,
-                                    double* __restrict__ out_v, uint8_t* __restrict__ rooted) {
+                                    double* __restrict__ out_v, uint8_t* __restrict__ rooted,
+                                    const long long* __restrict__ dtot) {
     const int lane = threadIdx.x & 31;
     const long long warp = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
     const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+    if (dtot) {  // asynchronous posts: output bases kept on the device
+        sbase = dtot[0];
+        vbase = dtot[1];
+    }
     for (long long i = warp; i < n; i += nwarps) {
         if (!valid[i]) continue;
         const long long o = vbase + voff[i];
@@ -223,10 +258,15 @@ __global__ void gather_joined_kernel(Rows slab_f, Rows slab_b,
                                      const long long* __restrict__ sidx, long long n,
                                      long long vbase, long long sbase,
                                      long long* __restrict__ out_off, double* __restrict__ out_v,
-                                     uint8_t* __restrict__ rooted) {
+                                     uint8_t* __restrict__ rooted,
+                                     const long long* __restrict__ dtot) {
     const int lane = threadIdx.x & 31;
     const long long warp = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
     const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+    if (dtot) {
+        sbase = dtot[0];
+        vbase = dtot[1];
+    }
     for (long long i = warp; i < n; i += nwarps) {
         if (!valid[i]) continue;
         const long long o = vbase + voff[i];
@@ -434,6 +474,7 @@ struct GrowSession {
     DevBuf export_ids;           // commits of the last batch (multi-rank mode)
     long long n_export = 0;
     long long nf_seeds = 0;      // field seeds selected by phg_grow_field_begin
+    DevBuf dtot;                 // [0] segments, [1] vertices, [2] never-entered snapshot
 };
 
 struct GrowCtx {  // per-call view
@@ -595,7 +636,7 @@ phg_status scalp_post(GrowCtx& G, Rows slab, const long long* keep, const uint8_
     gather_scalp_kernel<<<grid_for(nb * 32, 256, num_sms() * 16), 256, 0, G.st>>>(
         slab, keep, B.valid, B.voff, B.sidx, nb, S.verts,
         S.segs, c->g_out_off.as<long long>(), c->g_out_verts.as<double>(),
-        c->g_out_rooted.as<uint8_t>());
+        c->g_out_rooted.as<uint8_t>(), nullptr);
     PHG_CUDA(cudaGetLastError());
     S.segs += ns;
     S.verts += nv;
@@ -705,7 +746,8 @@ phg_status field_post(GrowCtx& G, Rows slab_f, const long long* keep_f,
     PHG_TRY(ensure_output(G, ns, nv));
     gather_joined_kernel<<<grid_for(nb * 32, 256, num_sms() * 16), 256, 0, G.st>>>(
         slab_f, slab_b, keep_f, keep_b, B.valid, B.voff, B.sidx, nb, S.verts, S.segs,
-        c->g_out_off.as<long long>(), c->g_out_verts.as<double>(), c->g_out_rooted.as<uint8_t>());
+        c->g_out_off.as<long long>(), c->g_out_verts.as<double>(), c->g_out_rooted.as<uint8_t>(),
+        nullptr);
     PHG_CUDA(cudaGetLastError());
     S.segs += ns;
     S.verts += nv;
@@ -814,6 +856,134 @@ long long spec_window(long long bs) {
     return w * bs;
 }
 
+// ---- optimistic windows: batch posts without host synchronisation -------------------------
+// Inside a speculative window the batches are posted back to back: segments, commits, offsets
+// and gathers all run on the stream, with the output bases kept on the device (S.dtot) and the
+// outputs preallocated for the whole window.  The host looks once per window.  A uint16 count
+// wrap (rare) makes the incremental cap plane unusable for the batches after it: the window is
+// then rolled back exactly (its commits undone, outputs and counters restored) and redone one
+// traced batch at a time, as the synchronous driver does after a wrap.
+
+// Post one scalp batch without synchronising (valid, commit, offsets, gather, totals).
+phg_status scalp_post_async(GrowCtx& G, Rows slab, const long long* keep, const uint8_t* ent,
+                            long long nb) {
+    GrowSession& S = *G.s;
+    phg_ctx* c = G.c;
+    BatchScratch B;
+    PHG_TRY(batch_scratch(G, nb, B));
+    segment_select_kernel<<<grid_for(nb, 256), 256, 0, G.st>>>(
+        keep, ent, nb, B.lens, B.segf, B.valid, S.misc.as<unsigned long long>());
+    PHG_CUDA(cudaGetLastError());
+    PHG_TRY(commit_batch(G, slab, keep, Rows{}, nullptr, B.valid, nb, 0, false));
+    PHG_TRY(scan_lengths(c, B.lens, nb, B.voff, G.st));
+    PHG_TRY(scan_lengths(c, B.segf, nb, B.sidx, G.st));
+    long long* dtot = S.dtot.as<long long>();
+    gather_scalp_kernel<<<grid_for(nb * 32, 256, num_sms() * 16), 256, 0, G.st>>>(
+        slab, keep, B.valid, B.voff, B.sidx, nb, 0, 0, c->g_out_off.as<long long>(),
+        c->g_out_verts.as<double>(), c->g_out_rooted.as<uint8_t>(), dtot);
+    advance_totals_kernel<<<1, 1, 0, G.st>>>(dtot, B.sidx + nb, B.voff + nb);
+    PHG_CUDA(cudaGetLastError());
+    return PHG_OK;
+}
+
+// Post one field batch (joins) without synchronising.
+phg_status field_post_async(GrowCtx& G, Rows slab_f, const long long* keep_f, const uint8_t* ent_f,
+                            Rows slab_b, const long long* keep_b, const uint8_t* ent_b,
+                            long long nb) {
+    GrowSession& S = *G.s;
+    phg_ctx* c = G.c;
+    BatchScratch B;
+    PHG_TRY(batch_scratch(G, nb, B));
+    join_select_kernel<<<grid_for(nb, 256), 256, 0, G.st>>>(keep_f, ent_f, keep_b, ent_b, nb,
+                                                            B.lens, B.segf, B.valid);
+    PHG_CUDA(cudaGetLastError());
+    PHG_TRY(commit_batch(G, slab_f, keep_f, slab_b, keep_b, B.valid, nb, 0, false));
+    PHG_TRY(scan_lengths(c, B.lens, nb, B.voff, G.st));
+    PHG_TRY(scan_lengths(c, B.segf, nb, B.sidx, G.st));
+    long long* dtot = S.dtot.as<long long>();
+    gather_joined_kernel<<<grid_for(nb * 32, 256, num_sms() * 16), 256, 0, G.st>>>(
+        slab_f, slab_b, keep_f, keep_b, B.valid, B.voff, B.sidx, nb, 0, 0,
+        c->g_out_off.as<long long>(), c->g_out_verts.as<double>(), c->g_out_rooted.as<uint8_t>(),
+        dtot);
+    advance_totals_kernel<<<1, 1, 0, G.st>>>(dtot, B.sidx + nb, B.voff + nb);
+    PHG_CUDA(cudaGetLastError());
+    return PHG_OK;
+}
+
+// Window start (after its trace): outputs sized by the trace's appended vertex counts (a kept
+// segment never has more), device totals = host totals, never-entered counter snapshot.
+phg_status window_begin(GrowCtx& G, long long add_segs, const TraceRecord& R, long long n) {
+    GrowSession& S = *G.s;
+    unsigned long long* sum = S.dtot.as<unsigned long long>() + 4;
+    PHG_CUDA(cudaMemsetAsync(sum, 0, 8, G.st));
+    sum_nverts_kernel<<<grid_for(n, 256, num_sms() * 8), 256, 0, G.st>>>(R.nverts, n, sum);
+    PHG_CUDA(cudaGetLastError());
+    PHG_CUDA(cudaMemcpyAsync(G.c->host_total, sum, 8, cudaMemcpyDeviceToHost, G.st));
+    PHG_CUDA(cudaStreamSynchronize(G.st));
+    PHG_TRY(ensure_output(G, add_segs, G.c->host_total[0]));
+    set_totals_kernel<<<1, 1, 0, G.st>>>(S.dtot.as<long long>(), S.segs, S.verts);
+    PHG_CUDA(cudaGetLastError());
+    PHG_CUDA(cudaMemcpyAsync(S.dtot.as<long long>() + 2, S.misc.p, 8, cudaMemcpyDeviceToDevice,
+                             G.st));
+    return PHG_OK;
+}
+
+// Window end (synchronises): adopt the device totals, or report a count wrap.
+phg_status window_end(GrowCtx& G, bool* wrapped) {
+    GrowSession& S = *G.s;
+    long long* h = G.c->host_total;
+    PHG_CUDA(cudaMemcpyAsync(h, S.dtot.p, 16, cudaMemcpyDeviceToHost, G.st));
+    PHG_CUDA(cudaMemcpyAsync(h + 2, S.misc.as<unsigned long long>() + 1, 8,
+                             cudaMemcpyDeviceToHost, G.st));
+    PHG_CUDA(cudaStreamSynchronize(G.st));
+    *wrapped = h[2] != 0;
+    if (!*wrapped) {
+        S.segs = h[0];
+        S.verts = h[1];
+    }
+    return PHG_OK;
+}
+
+// Undo one posted batch's commits exactly: its segments' distinct voxels, exported and
+// decremented.  valid is recomputed from the (truncated) keep arrays the post used.
+phg_status uncommit_batch(GrowCtx& G, Rows slab_a, const long long* keep_a, const uint8_t* ent_a,
+                          Rows slab_b, const long long* keep_b, const uint8_t* ent_b,
+                          long long nb) {
+    GrowSession& S = *G.s;
+    phg_ctx* c = G.c;
+    BatchScratch B;
+    PHG_TRY(batch_scratch(G, nb, B));
+    if (slab_b.base)
+        join_select_kernel<<<grid_for(nb, 256), 256, 0, G.st>>>(keep_a, ent_a, keep_b, ent_b, nb,
+                                                                B.lens, B.segf, B.valid);
+    else  // the never-entered count is restored from its window snapshot: count into a dummy
+        segment_select_kernel<<<grid_for(nb, 256), 256, 0, G.st>>>(
+            keep_a, ent_a, nb, B.lens, B.segf, B.valid, S.dtot.as<unsigned long long>() + 3);
+    PHG_CUDA(cudaGetLastError());
+    PHG_TRY(scan_lengths(c, B.lens, nb, B.voff, G.st));
+    PHG_CUDA(cudaMemcpyAsync(c->host_total, B.voff + nb, 8, cudaMemcpyDeviceToHost, G.st));
+    PHG_CUDA(cudaStreamSynchronize(G.st));
+    const long long nv = c->host_total[0];
+    const long long max_ids = nv + (slab_b.base ? nb : 0);
+    PHG_TRY(commit_batch(G, slab_a, keep_a, slab_b, keep_b, B.valid, nb, max_ids, true));
+    if (S.n_export)
+        uncommit_kernel<<<grid_for(S.n_export, 256, num_sms() * 16), 256, 0, G.st>>>(
+            S.export_ids.as<uint32_t>(), S.n_export, S.counts);
+    PHG_CUDA(cudaGetLastError());
+    S.n_export = 0;
+    return PHG_OK;
+}
+
+// After a wrap inside a window: counters back to the window start, cap plane to be rebuilt.
+phg_status window_restore(GrowCtx& G) {
+    GrowSession& S = *G.s;
+    PHG_CUDA(cudaMemcpyAsync(S.misc.p, S.dtot.as<long long>() + 2, 8, cudaMemcpyDeviceToDevice,
+                             G.st));
+    PHG_CUDA(cudaMemsetAsync(S.misc.as<unsigned long long>() + 1, 0, 8, G.st));
+    S.cap_valid = false;
+    return PHG_OK;
+}
+
 phg_status scalp_phase_spec(GrowCtx& G, const double* pos, const double* dir, long long n) {
     GrowSession& S = *G.s;
     phg_ctx* c = G.c;
@@ -827,26 +997,39 @@ phg_status scalp_phase_spec(GrowCtx& G, const double* pos, const double* dir, lo
         PHG_TRY(rec_buffers(G, nw, R));
         PHG_TRY(trace_core(c, S.f, &S.p, pos + 3 * w0, dir + 3 * w0, nw, nullptr, G.st, &R,
                            true));
+        PHG_TRY(window_begin(G, nw, R, nw));
+        const Rows rows = slab_rows(G);
+        const long long* keep = c->keep.as<long long>();
+        const uint8_t* ent = c->entered.as<uint8_t>();
         for (long long b0 = 0; b0 < nw; b0 += bs) {
             const long long nb = std::min(bs, nw - b0);
-            if (!S.cap_valid) {  // a count wrapped: trace every remaining batch afresh
-                for (long long r0 = w0 + b0; r0 < n; r0 += bs)
-                    PHG_TRY(scalp_batch(G, pos + 3 * r0, dir + 3 * r0, std::min(bs, n - r0),
-                                        false, &added));
-                return PHG_OK;
-            }
             if (b0 > 0) PHG_TRY(spec_truncate(G, R, b0, nb));  // the window's first batch saw
                                                                 // the plane it was traced with
-            PHG_TRY(scalp_post(G, slab_rows(G).sub(b0),
-                               c->keep.as<long long>() + b0, c->entered.as<uint8_t>() + b0, nb,
-                               false, &added));
+            PHG_TRY(scalp_post_async(G, rows.sub(b0), keep + b0, ent + b0, nb));
         }
+        bool wrapped = false;
+        PHG_TRY(window_end(G, &wrapped));
+        if (!wrapped) {
+            S.scalp_segs = S.segs;
+            continue;
+        }
+        // a count wrapped: undo the window, then trace every remaining batch afresh
+        for (long long b0 = 0; b0 < nw; b0 += bs) {
+            const long long nb = std::min(bs, nw - b0);
+            PHG_TRY(uncommit_batch(G, rows.sub(b0), keep + b0, ent + b0, Rows{}, nullptr, nullptr,
+                                   nb));
+        }
+        PHG_TRY(window_restore(G));
+        for (long long r0 = w0; r0 < n; r0 += bs)
+            PHG_TRY(scalp_batch(G, pos + 3 * r0, dir + 3 * r0, std::min(bs, n - r0), false,
+                                &added));
+        return PHG_OK;
     }
     return PHG_OK;
 }
 
 // every field batch (phg.py:277-302) the same way: one launch of all +d rows [0, nf) and -d
-// rows [nf, 2nf) against the plane after the scalp phase
+// rows [nf, 2nf) against the plane after the scalp phase, posted as one optimistic window
 phg_status field_phase_spec(GrowCtx& G) {
     GrowSession& S = *G.s;
     phg_ctx* c = G.c;
@@ -867,25 +1050,31 @@ phg_status field_phase_spec(GrowCtx& G) {
     TraceRecord R;
     PHG_TRY(rec_buffers(G, 2 * nf, R));
     PHG_TRY(trace_core(c, S.f, &S.p, pos2, dir2, 2 * nf, nullptr, G.st, &R, true));
+    PHG_TRY(window_begin(G, nf, R, 2 * nf));
     long long added = 0;
     const Rows slab = slab_rows(G);
     const long long* keep = c->keep.as<long long>();
     const uint8_t* ent = c->entered.as<uint8_t>();
     for (long long b0 = 0; b0 < nf; b0 += bs) {
         const long long nb = std::min(bs, nf - b0);
-        if (!S.cap_valid) {
-            for (long long r0 = b0; r0 < nf; r0 += bs)
-                PHG_TRY(field_batch(G, r0, std::min(bs, nf - r0), false, &added));
-            return PHG_OK;
-        }
         if (b0 > 0) {
             PHG_TRY(spec_truncate(G, R, b0, nb));
             PHG_TRY(spec_truncate(G, R, nf + b0, nb));
         }
-        PHG_TRY(field_post(G, slab.sub(b0), keep + b0, ent + b0,
-                           slab.sub(nf + b0), keep + nf + b0, ent + nf + b0, nb,
-                           false, &added));
+        PHG_TRY(field_post_async(G, slab.sub(b0), keep + b0, ent + b0, slab.sub(nf + b0),
+                                 keep + nf + b0, ent + nf + b0, nb));
     }
+    bool wrapped = false;
+    PHG_TRY(window_end(G, &wrapped));
+    if (!wrapped) return PHG_OK;
+    for (long long b0 = 0; b0 < nf; b0 += bs) {
+        const long long nb = std::min(bs, nf - b0);
+        PHG_TRY(uncommit_batch(G, slab.sub(b0), keep + b0, ent + b0, slab.sub(nf + b0),
+                               keep + nf + b0, ent + nf + b0, nb));
+    }
+    PHG_TRY(window_restore(G));
+    for (long long r0 = 0; r0 < nf; r0 += bs)
+        PHG_TRY(field_batch(G, r0, std::min(bs, nf - r0), false, &added));
     return PHG_OK;
 }
 
@@ -932,6 +1121,8 @@ phg_status phg_grow_begin(phg_ctx* c, phg_field* f, const phg_params_v1* p,
     PHG_CUDA(cudaMemsetAsync(c->counters.p, 0, 64, st));
     PHG_TRY(S.misc.ensure(64));
     PHG_CUDA(cudaMemsetAsync(S.misc.p, 0, 64, st));
+    PHG_TRY(S.dtot.ensure(64));
+    PHG_CUDA(cudaMemsetAsync(S.dtot.p, 0, 64, st));
     PHG_CUDA(cudaStreamSynchronize(st));  // host counts may be released after return
     return PHG_OK;
 }
