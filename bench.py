@@ -106,6 +106,8 @@ def binding_resource():
             "l1_wavefronts": pct("l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed"),
             "dram": pct("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"),
             "inst_per_step": d.get("inst_per_step"),
+            "gather_gbs": d.get("gather_gbs"),
+            "ld_sectors_per_request": d.get("ld_sectors_per_request"),
             "stalls_per_issue": d.get("stalls_per_issue"),
             "source": "profiles/ncu_trace_summary.json (ncu --set full, C3)"}
 

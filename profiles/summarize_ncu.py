@@ -66,6 +66,16 @@ def main(rep, out, label, cmd, steps):
          "st_sectors_per_request": _ratio(v, col, "l1tex__t_sectors_pipe_lsu_mem_global_op_st.sum",
                                           "l1tex__t_requests_pipe_lsu_mem_global_op_st.sum"),
          "stalls_per_issue": dict(sorted(stalls.items(), key=lambda kv: -kv[1])), "metrics": m}
+    # where the corner gathers are served: sectors x 32 B over the kernel duration
+    try:
+        t = float(v[col["gpu__time_duration.sum"]]) * {"ms": 1e-3, "us": 1e-6, "s": 1.0}[
+            u[col["gpu__time_duration.sum"]]]
+        l1 = float(v[col["l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum"]]) * 32
+        l2 = float(v[col["lts__t_sectors_srcunit_tex_op_read.sum"]]) * 32
+        d["gather_gbs"] = {"l1_load_sectors": l1 / t / 1e9, "l2_read_from_l1": l2 / t / 1e9,
+                           "dram_read": dr / t / 1e9, "dram_write": dw / t / 1e9}
+    except (KeyError, ValueError):
+        pass
     with open(out, "w") as f:
         json.dump(d, f, indent=1)
     print(json.dumps({k: d[k] for k in ("dram_bytes_per_step", "inst_per_step",
