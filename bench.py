@@ -376,7 +376,8 @@ def run_ours(args):
                        "seeds_per_gpu": per_rank, "global_seeds": per_rank * ws,
                        "max_vertices": params.max_vertices, "step_mm": params.step_mm,
                        "batch_size": per_rank * ws, "parallelism": f"seed-partition x{ws}",
-                       "l2": "256 MiB flush write between timed steps; field 2 GiB > L2"},
+                       "l2": f"256 MiB flush write between timed steps; packed field "
+                             f"{(cfg.n + 2) ** 3 * 16 / 2 ** 30:.1f} GiB > L2"},
             "steps_per_trace": steps_per_trace, "accepted_steps_per_trace": accepted,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
