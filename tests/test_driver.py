@@ -105,6 +105,42 @@ def test_device_driver_prefilled_counts_and_uint16_wrap(oracle_c):
     assert (counts < init).any()  # some voxel really wrapped
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("scalp_inside", [False, True])
+def test_device_driver_wrap_in_field_window(oracle_c, scalp_inside):
+    """A uint16 wrap inside the field pass's optimistic window (and, with scalp seeds inside
+    the volume, in both passes): the window is rolled back and redone batch by batch, and the
+    result must still equal the oracle bit for bit (segments, counts, report).  The cap is
+    unreachable for uint16 counts, so strands cross the pre-filled 65535 voxels and wrap them;
+    scalp seeds below the volume never enter, so every commit comes from the field pass."""
+    from oracle import phg_driver_np as dn
+    from paper_2604_05794_b200 import grow, synth
+    from paper_2604_05794_b200.volume import OOVolume
+
+    ori, occ = synth.make_field("curly", 40, "cpu")
+    ori, occ = ori.numpy(), occ.numpy()
+    rng = np.random.Generator(np.random.Philox(key=91))
+    init = rng.choice(np.array([0, 0, 0, 0, 1, 65535], np.uint16), size=occ.shape)
+    seeds, dirs = synth.disk_seeds(40, 600, 43)
+    if not scalp_inside:
+        seeds = seeds - np.array([0.0, 0.0, 500.0])  # below the volume: never entered
+    params = _params(dict(batch_size=64, occupancy_cap=100000, field_seeds=900, max_vertices=120))
+    vol = OOVolume.empty((0, 0, 0), synth.VOXEL_MM, occ.shape)
+    vol.occ, vol.ori, vol.counts = occ, ori, init.copy()
+    segs, rep = grow.init_guide_strands(SimpleNamespace(seeds=seeds, seed_normals=dirs), vol,
+                                        params)
+    counts = init.copy()
+    out, rep_o = dn.init_guide(np.zeros(3), synth.VOXEL_MM, occ, ori, counts, seeds, dirs, params)
+    assert np.array_equal(vol.counts, counts)
+    assert rep == rep_o
+    off, verts, rooted = _csr([(s.vertices, s.rooted) for s in segs])
+    off_o, verts_o, rooted_o = _csr(out)
+    assert np.array_equal(off, off_o) and np.array_equal(verts, verts_o)
+    assert np.array_equal(rooted, rooted_o)
+    assert (counts < init).any()  # some voxel really wrapped
+    assert (~rooted_o).sum() > 0  # the field pass produced segments
+
+
 def _driver_vs_oracle(kind, n, nseeds, key, radius_frac=0.4, **pkw):
     from oracle import phg_driver_np as dn
     from paper_2604_05794_b200 import grow, synth
