@@ -11,7 +11,8 @@ Steps are counted as the reference counts them: sum over returned strands of
 
 Multi-GPU: one process per GPU (torchrun), field replicated, seeds of the
 global batch partitioned in contiguous rank slices, per-GPU seed count fixed
-("weak" scaling).  Rank 0 prints one JSON line.
+("weak" scaling); --config C4 instead splits BASELINE's 4M global seeds over the
+ranks ("strong" scaling).  Rank 0 prints one JSON line.
 """
 
 from __future__ import annotations
@@ -260,7 +261,10 @@ def run_ours(args):
     if ws > 1:
         dist.init_process_group("nccl", device_id=dev)
     cfg = synth.CONFIGS[args.config]
-    per_rank = args.seeds or cfg.seeds
+    # C4 is BASELINE's scaling sweep: 4M global seeds split over the ranks (strong scaling);
+    # every other config fixes the seeds per GPU (weak scaling)
+    strong = cfg.name == "C4" and not args.seeds
+    per_rank = args.seeds or (cfg.seeds // ws if strong else cfg.seeds)
     params = phg.PhgParams(field_seeds=0, batch_size=per_rank * ws)
 
     # field generated directly in HBM, packed once (replicated per rank)
@@ -370,7 +374,8 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong" if strong else "weak",
+            "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
             "config": {"workload": f"{cfg.name}: {cfg.note}", "field": f"{cfg.n}^3 {cfg.kind}",
                        "seeds_per_gpu": per_rank, "global_seeds": per_rank * ws,
@@ -580,15 +585,26 @@ def e2e_leg(args, tracer, field, params, s_host, d_host, per_rank, ws, dev, step
     import torch
     import torch.distributed as dist
 
-    pin_s = torch.from_numpy(s_host).pin_memory()
-    pin_d = torch.from_numpy(d_host).pin_memory()
     n = per_rank
-    out_off = torch.empty(n + 1, dtype=torch.int64).pin_memory()
-    out_ent = torch.empty(n, dtype=torch.uint8).pin_memory()
     stream = torch.cuda.current_stream(dev)
-    total = tracer.trace(field, params, pin_s.data_ptr(), pin_d.data_ptr(), n,
-                         out_off.data_ptr(), out_ent.data_ptr(), None, stream.cuda_stream)
-    out_v = torch.empty((total, 3), dtype=torch.float64).pin_memory()
+    err = None
+    try:  # every rank pins ~24 B x its output vertices; agree on success before any collective
+        pin_s = torch.from_numpy(s_host).pin_memory()
+        pin_d = torch.from_numpy(d_host).pin_memory()
+        out_off = torch.empty(n + 1, dtype=torch.int64).pin_memory()
+        out_ent = torch.empty(n, dtype=torch.uint8).pin_memory()
+        total = tracer.trace(field, params, pin_s.data_ptr(), pin_d.data_ptr(), n,
+                             out_off.data_ptr(), out_ent.data_ptr(), None, stream.cuda_stream)
+        out_v = torch.empty((total, 3), dtype=torch.float64).pin_memory()
+    except (RuntimeError, MemoryError) as exc:
+        err = str(exc).splitlines()[0][:200] if str(exc) else type(exc).__name__
+    if ws > 1:
+        ok = torch.tensor([0 if err else 1], dtype=torch.int32, device=dev)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if not ok.item() and err is None:
+            err = "another rank could not allocate its pinned host buffers"
+    if err is not None:
+        return {"value": None, "unit": "steps/s", "error": err}
 
     def one():
         # phg_trace_to_host: chunked, the D2H of chunk k overlaps the trace of chunk k+1
