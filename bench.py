@@ -272,7 +272,7 @@ def run_ours(args):
     field = DeviceField(np.zeros(3), synth.VOXEL_MM, occ, ori,
                         torch.cuda.current_stream(dev).cuda_stream)
     ori_host = occ_host = None
-    if rank == 0 and not args.no_cpu:
+    if ws == 1 and not args.no_cpu:
         ori_host, occ_host = ori.cpu().numpy(), occ.cpu().numpy()
     all_seeds, all_dirs = synth.config_seeds(cfg, per_rank * ws, ori, occ)
     del ori, occ
@@ -355,7 +355,7 @@ def run_ours(args):
         traffic = traffic * accepted / traffic_steps
 
     cpu = None
-    if rank == 0 and not args.no_cpu:
+    if ws == 1 and not args.no_cpu:  # the CPU baseline is an N=1 figure (rank 0 only)
         cores, model = cpu_host_info()
         sample = args.cpu_sample or max(1024, cores * 256)
         s_cpu, t_cpu = cpu_numpy_port(ori_host, occ_host, s_host[:sample], d_host[:sample],
