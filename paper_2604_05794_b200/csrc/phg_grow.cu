@@ -633,7 +633,7 @@ phg_status scalp_post(GrowCtx& G, Rows slab, const long long* keep, const uint8_
     if (export_commits)
         PHG_TRY(commit_batch(G, slab, keep, Rows{}, nullptr, B.valid, nb, nv, true));
     PHG_TRY(ensure_output(G, ns, nv));
-    gather_scalp_kernel<<<grid_for(nb * 32, 256, num_sms() * 16), 256, 0, G.st>>>(
+    gather_scalp_kernel<<<grid_for(nb * 32, 256, num_sms() * kCopyCtasPerSm), 256, 0, G.st>>>(
         slab, keep, B.valid, B.voff, B.sidx, nb, S.verts,
         S.segs, c->g_out_off.as<long long>(), c->g_out_verts.as<double>(),
         c->g_out_rooted.as<uint8_t>(), nullptr);
@@ -744,7 +744,7 @@ phg_status field_post(GrowCtx& G, Rows slab_f, const long long* keep_f,
     if (export_commits)
         PHG_TRY(commit_batch(G, slab_f, keep_f, slab_b, keep_b, B.valid, nb, nv + ns, true));
     PHG_TRY(ensure_output(G, ns, nv));
-    gather_joined_kernel<<<grid_for(nb * 32, 256, num_sms() * 16), 256, 0, G.st>>>(
+    gather_joined_kernel<<<grid_for(nb * 32, 256, num_sms() * kCopyCtasPerSm), 256, 0, G.st>>>(
         slab_f, slab_b, keep_f, keep_b, B.valid, B.voff, B.sidx, nb, S.verts, S.segs,
         c->g_out_off.as<long long>(), c->g_out_verts.as<double>(), c->g_out_rooted.as<uint8_t>(),
         nullptr);
@@ -878,7 +878,7 @@ phg_status scalp_post_async(GrowCtx& G, Rows slab, const long long* keep, const 
     PHG_TRY(scan_lengths(c, B.lens, nb, B.voff, G.st));
     PHG_TRY(scan_lengths(c, B.segf, nb, B.sidx, G.st));
     long long* dtot = S.dtot.as<long long>();
-    gather_scalp_kernel<<<grid_for(nb * 32, 256, num_sms() * 16), 256, 0, G.st>>>(
+    gather_scalp_kernel<<<grid_for(nb * 32, 256, num_sms() * kCopyCtasPerSm), 256, 0, G.st>>>(
         slab, keep, B.valid, B.voff, B.sidx, nb, 0, 0, c->g_out_off.as<long long>(),
         c->g_out_verts.as<double>(), c->g_out_rooted.as<uint8_t>(), dtot);
     advance_totals_kernel<<<1, 1, 0, G.st>>>(dtot, B.sidx + nb, B.voff + nb);
@@ -901,7 +901,7 @@ phg_status field_post_async(GrowCtx& G, Rows slab_f, const long long* keep_f, co
     PHG_TRY(scan_lengths(c, B.lens, nb, B.voff, G.st));
     PHG_TRY(scan_lengths(c, B.segf, nb, B.sidx, G.st));
     long long* dtot = S.dtot.as<long long>();
-    gather_joined_kernel<<<grid_for(nb * 32, 256, num_sms() * 16), 256, 0, G.st>>>(
+    gather_joined_kernel<<<grid_for(nb * 32, 256, num_sms() * kCopyCtasPerSm), 256, 0, G.st>>>(
         slab_f, slab_b, keep_f, keep_b, B.valid, B.voff, B.sidx, nb, 0, 0,
         c->g_out_off.as<long long>(), c->g_out_verts.as<double>(), c->g_out_rooted.as<uint8_t>(),
         dtot);

@@ -20,6 +20,7 @@ no CPU fallback: without the native library every call raises PipelineError.
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -180,13 +181,41 @@ def trace_batch_csr(vol, seed_pos, seed_dir, params, at_cap=None, live_counts=No
     offsets = np.zeros(n + 1, np.int64)
     entered = np.zeros(n, np.uint8)
     tr = _tracer()
-    total = tr.trace(field, params, pos.ctypes.data if n else None,
-                     dirs.ctypes.data if n else None, n, offsets.ctypes.data,
-                     entered.ctypes.data if n else None, counts_ptr)
-    verts = np.empty((total, 3))
-    if total:
-        tr.gather(verts.ctypes.data, total)
-    return offsets, verts, entered.astype(bool)
+    chunk = n if strict else max(1, min(n, slab_budget_bytes() // slab_row_bytes(params)))
+    if chunk >= n:
+        total = tr.trace(field, params, pos.ctypes.data if n else None,
+                         dirs.ctypes.data if n else None, n, offsets.ctypes.data,
+                         entered.ctypes.data if n else None, counts_ptr)
+        verts = np.empty((total, 3))
+        if total:
+            tr.gather(verts.ctypes.data, total)
+        return offsets, verts, entered.astype(bool)
+    # Relaxed strands are independent (the cap plane is fixed for the call), so a seed set
+    # whose trace slab would not fit the budget is traced in seed-order chunks: bit-identical
+    # to one call, with the slab bounded instead of n * max_vertices * 24 bytes.
+    parts, base = [], 0
+    for s0 in range(0, n, chunk):
+        s1 = min(n, s0 + chunk)
+        off_k = np.zeros(s1 - s0 + 1, np.int64)
+        mk = tr.trace(field, params, pos[s0:s1].ctypes.data, dirs[s0:s1].ctypes.data, s1 - s0,
+                      off_k.ctypes.data, entered[s0:].ctypes.data, None)
+        v = np.empty((mk, 3))
+        if mk:
+            tr.gather(v.ctypes.data, mk)
+        offsets[s0:s1 + 1] = off_k + base
+        parts.append(v)
+        base += mk
+    return offsets, np.concatenate(parts), entered.astype(bool)
+
+
+def slab_row_bytes(params):
+    """Bytes of one strand's trace-slab row (phg_core.cuh row_stride_doubles)."""
+    return ((int(params.max_vertices) + 3) & ~3) * 24
+
+
+def slab_budget_bytes():
+    """Cap on the relaxed trace slab of one trace_batch call (PHG_SLAB_BUDGET_GB, default 24)."""
+    return int(float(os.environ.get("PHG_SLAB_BUDGET_GB", "24")) * (1 << 30))
 
 
 def trace_batch(vol, seed_pos, seed_dir, params, at_cap=None, live_counts=None, near_occ=None):

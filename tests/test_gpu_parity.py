@@ -249,6 +249,17 @@ def test_seed_order_does_not_change_results(gpu):
         assert e[i] == e2[k]
 
 
+def test_slab_budget_chunking_is_bit_identical(gpu, monkeypatch):
+    """A seed set whose relaxed trace slab exceeds PHG_SLAB_BUDGET_GB is traced in seed-order
+    chunks; offsets, vertices and entered flags equal the single-call result."""
+    vol, s, d, p = _config_case("sparse", 64, 6_000, 18, interior=1_000)
+    off, v, e = gpu.phg.trace_batch_csr(vol, s, d, p)
+    row = gpu.phg.slab_row_bytes(p)
+    monkeypatch.setenv("PHG_SLAB_BUDGET_GB", str(1_777 * row / (1 << 30)))  # 4 ragged chunks
+    off2, v2, e2 = gpu.phg.trace_batch_csr(vol, s, d, p)
+    assert np.array_equal(off, off2) and np.array_equal(v, v2) and np.array_equal(e, e2)
+
+
 # ---- the reference's own trace tests, run against the GPU drop-in ---------------------
 def _column(height=40):
     from paper_2604_05794_b200.volume import OOVolume
