@@ -77,6 +77,19 @@ def test_params_mirror_validation():
             p.min_support, p.coast_steps) == (1.0, 400, 16384, 16, 24, 0.05, 25)
 
 
+def test_slab_row_bytes_matches_device_row_stride(monkeypatch):
+    """phg.slab_row_bytes mirrors row_stride_doubles (phg_core.cuh): rows padded to 4 vertices
+    (96 B), so the chunked drop-in sizes its slab exactly as the C ABI allocates it."""
+    from paper_2604_05794_b200 import phg
+
+    src = open(os.path.join(ROOT, "paper_2604_05794_b200", "csrc", "phg_core.cuh")).read()
+    assert re.search(r"\(max_vertices \+ 3\) & ~3\) \* 3", src)
+    for mv, want in ((1, 96), (4, 96), (5, 192), (400, 9600), (401, 9696)):
+        assert phg.slab_row_bytes(phg.PhgParams(max_vertices=mv)) == want
+    monkeypatch.setenv("PHG_SLAB_BUDGET_GB", "0.5")
+    assert phg.slab_budget_bytes() == 1 << 29
+
+
 def test_product_package_never_imports_oracle():
     pkg = os.path.join(ROOT, "paper_2604_05794_b200")
     for dirpath, _, files in os.walk(pkg):
