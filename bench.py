@@ -345,6 +345,10 @@ def run_ours(args):
         driver = driver_leg(cfg, field, s_host, d_host, dev)
         a9 = a9_leg()
     if not args.no_e2e and ws == 1 and ori_host is not None:
+        # the drop-in runs on its own context: release the timed context's slab and CSR
+        # scratch first (C4's 4M seeds hold ~77 GB there)
+        tracer.close()
+        torch.cuda.empty_cache()
         dropin = dropin_leg(ori_host, occ_host, s_host, d_host, params)
 
     kernel_ms = float(np.mean(kern_ms))
