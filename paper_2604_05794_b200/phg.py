@@ -193,19 +193,29 @@ def trace_batch_csr(vol, seed_pos, seed_dir, params, at_cap=None, live_counts=No
     # Relaxed strands are independent (the cap plane is fixed for the call), so a seed set
     # whose trace slab would not fit the budget is traced in seed-order chunks: bit-identical
     # to one call, with the slab bounded instead of n * max_vertices * 24 bytes.
-    parts, base = [], 0
+    # Each chunk's vertices are gathered straight into their final rows of one host array,
+    # sized from the first chunk's yield (+25%; untouched tail pages are never committed) and
+    # regrown by copy only if a later chunk overruns it.
+    verts, base = None, 0
     for s0 in range(0, n, chunk):
         s1 = min(n, s0 + chunk)
         off_k = np.zeros(s1 - s0 + 1, np.int64)
         mk = tr.trace(field, params, pos[s0:s1].ctypes.data, dirs[s0:s1].ctypes.data, s1 - s0,
                       off_k.ctypes.data, entered[s0:].ctypes.data, None)
-        v = np.empty((mk, 3))
-        if mk:
-            tr.gather(v.ctypes.data, mk)
         offsets[s0:s1 + 1] = off_k + base
-        parts.append(v)
+        if verts is None:
+            verts = np.empty((max(mk, int(mk * n / (s1 - s0) * _CHUNK_HEADROOM) + 1024), 3))
+        elif base + mk > len(verts):
+            grown = np.empty((max(base + mk, 2 * len(verts)), 3))
+            grown[:base] = verts[:base]
+            verts = grown
+        if mk:
+            tr.gather(verts[base:].ctypes.data, mk)
         base += mk
-    return offsets, np.concatenate(parts), entered.astype(bool)
+    return offsets, verts[:base], entered.astype(bool)
+
+
+_CHUNK_HEADROOM = 1.25  # host CSR sizing factor over the first chunk's vertices per seed
 
 
 def slab_row_bytes(params):

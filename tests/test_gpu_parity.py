@@ -258,6 +258,9 @@ def test_slab_budget_chunking_is_bit_identical(gpu, monkeypatch):
     monkeypatch.setenv("PHG_SLAB_BUDGET_GB", str(1_777 * row / (1 << 30)))  # 4 ragged chunks
     off2, v2, e2 = gpu.phg.trace_batch_csr(vol, s, d, p)
     assert np.array_equal(off, off2) and np.array_equal(v, v2) and np.array_equal(e, e2)
+    monkeypatch.setattr(gpu.phg, "_CHUNK_HEADROOM", 0.01)  # host array regrown mid-call
+    off3, v3, e3 = gpu.phg.trace_batch_csr(vol, s, d, p)
+    assert np.array_equal(off, off3) and np.array_equal(v, v3) and np.array_equal(e, e3)
 
 
 # ---- the reference's own trace tests, run against the GPU drop-in ---------------------
