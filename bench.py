@@ -1,18 +1,19 @@
-"""PHG strand-vertex steps/s on B200 (BASELINE.json metric; workload C3 by default).
+"""PHG strand-vertex steps/s on B200 (BASELINE.json metric).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C3]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config Cx]
 
 One step = one trace of this rank's seed batch: every seed
 integrated to termination through the field, kept vertices scanned and
 gathered into the CSR payload (K1 + K2), plus -- at N > 1 -- the final
 all-gather of per-rank (strands, vertices) that yields global CSR offsets.
 Steps are counted as the reference counts them: sum over returned strands of
-(len(vertices) - 1).
+(len(vertices) - 1), summed over every rank.
 
-Multi-GPU: one process per GPU (torchrun), field replicated, seeds of the
-global batch partitioned in contiguous rank slices, per-GPU seed count fixed
-("weak" scaling); --config C4 instead splits BASELINE's 4M global seeds over the
-ranks ("strong" scaling).  Rank 0 prints one JSON line.
+Workload: C3 (512^3 curly field, 1M seeds) at one GPU, the config BASELINE.json's
+metric is quoted on; at N > 1 the default is C4, BASELINE's scaling sweep: 4M
+global seeds split over the ranks ("strong" scaling).  --config C3 at N > 1 fixes
+1M seeds per GPU ("weak").  One process per GPU (torchrun), field replicated,
+contiguous rank slices of the seed list.  Rank 0 prints one JSON line.
 """
 
 from __future__ import annotations
@@ -40,7 +41,11 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="C3")
+    ap.add_argument("--config", default=None,
+                    help="C1..C5 (default: C3 at one GPU, C4's 4M-seed strong split at N > 1)")
+    ap.add_argument("--dist-backend", default="auto", choices=["auto", "nccl", "gloo"],
+                    help="auto: NCCL when every rank has its own GPU, else gloo (ranks sharing a "
+                         "device: code-path validation only, not a scaling measurement)")
     ap.add_argument("--seeds", type=int, default=0, help="override seeds per rank")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -60,6 +65,14 @@ def _native_variants():
     return int(_native.load().phg_num_variants())
 
 
+def resolve_config(args, ws):
+    """BASELINE.json: the metric is quoted on C3 (512^3, 1M seeds) at one GPU; its scaling
+    sweep is C4 (512^3, 4M seeds partitioned across 2/4/8 GPUs)."""
+    if args.config is None:
+        args.config = "C3" if ws == 1 else "C4"
+    return args.config
+
+
 def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -73,44 +86,6 @@ def measured_peak():
             return float(json.load(f)["hbm_gbs"]), "measured"
     except Exception:  # noqa: BLE001
         return 6650.0, "fallback (B200_PROFILING.md)"
-
-
-def ncu_summary():
-    try:
-        with open(os.path.join(ROOT, "profiles", "ncu_trace_summary.json")) as f:
-            return json.load(f)
-    except Exception:  # noqa: BLE001
-        return {}
-
-
-def ncu_traffic():
-    """Per-launch DRAM bytes of the trace kernel from the committed ncu summary, if any."""
-    d = ncu_summary()
-    return d.get("dram_bytes_per_launch"), d.get("steps_per_launch")
-
-
-def binding_resource():
-    """What actually bounds the trace kernel per the committed ncu capture: the gathers are
-    L1/L2-resident, so DRAM is far from busy; issue slots and the fp64 pipe are the limits."""
-    m = ncu_summary().get("metrics", {})
-
-    def pct(k):
-        try:
-            return float(m[k][0]) / 100.0
-        except Exception:  # noqa: BLE001
-            return None
-
-    d = ncu_summary()
-    return {"issue_active": pct("smsp__issue_active.avg.pct_of_peak_sustained_active"),
-            "fp64_pipe": pct("sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active"),
-            "xu_pipe": pct("sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active"),
-            "l1_wavefronts": pct("l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed"),
-            "dram": pct("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"),
-            "inst_per_step": d.get("inst_per_step"),
-            "gather_gbs": d.get("gather_gbs"),
-            "ld_sectors_per_request": d.get("ld_sectors_per_request"),
-            "stalls_per_issue": d.get("stalls_per_issue"),
-            "source": "profiles/ncu_trace_summary.json (ncu --set full, C3)"}
 
 
 class ClockSampler:
@@ -183,22 +158,82 @@ def cpu_host_info():
     return cores, model
 
 
-def cpu_numpy_port(ori, occ, seeds, dirs, params, workers):
-    """The reference's algorithm as the reference runs it (numpy, fork pool) -- oracle port."""
-    from oracle import phg_oracle_np as onp  # CPU baseline leg only
+CPU_SUBSET = 16384  # C2-C5 are timed on the first 16384 seeds, C1 on all
 
-    f = onp.Field(np.zeros(3), 2.0, occ.shape, occ, ori)
+
+def cpu_sample_seeds(cfg, args, ori_t=None, occ_t=None):
+    """The CPU legs' seeds: the first 16384 of the config's own seed list (all of C1's 10k),
+    BASELINE.md 2; --cpu-sample overrides."""
+    from paper_2604_05794_b200 import synth
+
+    n = args.cpu_sample or (cfg.seeds if cfg.name == "C1" else CPU_SUBSET)
+    n = min(n, cfg.seeds)
+    seeds, dirs = synth.config_seeds(cfg, cfg.seeds, ori_t, occ_t)  # the workload's own list
+    return np.ascontiguousarray(seeds[:n]), np.ascontiguousarray(dirs[:n])
+
+
+def cpu_sample_note(cfg, n):
+    return (f"all {n} seeds of {cfg.name}" if n >= cfg.seeds
+            else f"first {n} seeds of {cfg.name}")
+
+
+def cpu_legs(cfg, ori, occ, seeds, dirs, cores, model, one_core=True, c_port=True):
+    """BASELINE.md 2's CPU baseline on this host, on the config's CPU sample:
+      * value: the numpy restatement of trace_batch (bit-exact to the reference, the same
+        numpy dispatch pattern) in a persistent `cores`-process fork pool -- the most
+        CPU-favourable form of the reference's own multi-core path;
+      * init_guide_strands: the reference's multi-core path as `strandkit bench` times it
+        (cli.py:233-237): init_guide_strands(workers=cores, field_seeds=0), pool made per
+        call, serial commit loop (phg.py:210-260);
+      * one_core: trace_batch in one process (BASELINE.md 2 (i));
+      * c_port: our scalar C restatement on all threads (not the reference; context only)."""
+    from types import SimpleNamespace
+
+    from oracle import phg_oracle_np as onp  # CPU baseline legs only
+
+    from paper_2604_05794_b200 import synth
+    from paper_2604_05794_b200.phg import PhgParams
+
+    params = PhgParams(field_seeds=0, batch_size=max(len(seeds), 1))
+    f = onp.Field(np.zeros(3), synth.VOXEL_MM, occ.shape, occ, ori)
+    out = {"unit": "steps/s", "cores": cores, "kind": "port"}
+    pool = onp.TracePool(f, cores)
+    try:
+        pool.steps(seeds[: cores * 64], dirs[: cores * 64], params)  # warm the workers
+        t0 = time.perf_counter()
+        st = pool.steps(seeds, dirs, params)
+        out["value"] = st / (time.perf_counter() - t0)
+    finally:
+        pool.close()
+    out["sample"] = (f"{cpu_sample_note(cfg, len(seeds))}: numpy restatement of trace_batch "
+                     f"(bit-exact to the reference) in a persistent {cores}-process fork pool, "
+                     f"{len(seeds) // cores} seeds per worker (phg.py:201 slicing); host {model}")
+    counts = np.zeros(occ.shape, np.uint16)
+    ig = PhgParams(field_seeds=0)  # reference defaults: batch 16384, cap 16
     t0 = time.perf_counter()
-    steps = onp.steps_multicore(f, seeds, dirs, params, workers=workers)
-    return steps, time.perf_counter() - t0
+    segs, st = onp.init_guide_strands_scalp(f, counts, seeds, dirs, ig, cores)
+    dt = time.perf_counter() - t0
+    out["init_guide_strands"] = {
+        "value": st / dt, "seconds": dt, "steps": int(st), "segments": len(segs),
+        "what": f"port of init_guide_strands(workers={cores}, field_seeds=0) as strandkit "
+                "bench times it (cli.py:233-237): pool made per call, batch 16384, serial "
+                "per-segment commit loop"}
+    if one_core:
+        t0 = time.perf_counter()
+        _, keep, _ = onp.trace(f, seeds, dirs, params)
+        dt = time.perf_counter() - t0
+        out["one_core"] = {"value": int((keep - 1).sum()) / dt, "seconds": dt,
+                           "what": "trace_batch port in one process (BASELINE.md 2 (i))"}
+    if c_port:
+        from oracle import phg_oracle_c as oc  # CPU baseline legs only
 
-
-def cpu_c_port(ori, occ, seeds, dirs, params, threads):
-    from oracle import phg_oracle_c as oc  # CPU baseline leg only
-
-    t0 = time.perf_counter()
-    _, keep, _ = oc.trace(np.zeros(3), 2.0, occ, ori, seeds, dirs, params, threads=threads)
-    return int((keep - 1).sum()), time.perf_counter() - t0
+        t0 = time.perf_counter()
+        _, keep, _ = oc.trace(np.zeros(3), synth.VOXEL_MM, occ, ori, seeds, dirs, params,
+                              threads=cores)
+        out["c_port_value"] = int((keep - 1).sum()) / (time.perf_counter() - t0)
+        out["c_port_sample"] = (f"same seeds, our scalar C restatement on {cores} OpenMP "
+                                "threads (context: not the reference's code)")
+    return out
 
 
 def host_field(cfg):
@@ -216,21 +251,27 @@ def run_reference(args):
     from paper_2604_05794_b200 import synth
     from paper_2604_05794_b200.phg import PhgParams
 
-    cfg = synth.CONFIGS[args.config]
+    cfg = synth.CONFIGS[resolve_config(args, ws)]
     cores, model = cpu_host_info()
     params = PhgParams(field_seeds=0)
-    ori, occ = host_field(cfg)
-    sample = args.cpu_sample or max(1024, cores * 256)
-    seeds, dirs = synth.disk_seeds(cfg.n, cfg.seeds * max(ws, 1), cfg.key)
-    seeds, dirs = seeds[:sample], dirs[:sample]
-    for _ in range(max(args.warmup, 0) and 1):
-        cpu_numpy_port(ori, occ, seeds[: cores * 8], dirs[: cores * 8], params, cores)
-    rates, tot_t, tot_s = [], 0.0, 0
-    for _ in range(args.steps):
-        s, t = cpu_numpy_port(ori, occ, seeds, dirs, params, cores)
-        rates.append(s / t)
-        tot_t += t
-        tot_s += s
+    ori_t, occ_t = synth.make_field(cfg.kind, cfg.n, "cpu")
+    seeds, dirs = cpu_sample_seeds(cfg, args, ori_t, occ_t)
+    ori, occ = ori_t.numpy(), occ_t.numpy()
+    del ori_t, occ_t
+    from oracle import phg_oracle_np as onp  # the reference arm: the port, on host cores
+
+    f = onp.Field(np.zeros(3), synth.VOXEL_MM, occ.shape, occ, ori)
+    pool = onp.TracePool(f, cores)
+    try:
+        for _ in range(min(max(args.warmup, 0), 1)):
+            pool.steps(seeds[: cores * 64], dirs[: cores * 64], params)
+        tot_t, tot_s = 0.0, 0
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            tot_s += pool.steps(seeds, dirs, params)
+            tot_t += time.perf_counter() - t0
+    finally:
+        pool.close()
     v = tot_s / tot_t
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": v, "unit": "steps/s", "n_gpus": ws,
@@ -238,13 +279,138 @@ def run_reference(args):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
         "config": {"workload": f"{cfg.name}: {cfg.note}", "sample_seeds": int(len(seeds)),
-                   "field": f"{cfg.n}^3 {cfg.kind}"},
+                   "field": f"{cfg.n}^3 {cfg.kind}",
+                   "seeds_per_worker": int(len(seeds)) // cores},
         "cpu_baseline": {"value": v, "unit": "steps/s", "cores": cores, "kind": "port",
-                         "sample": f"first {len(seeds)} seeds of {cfg.name} per step, numpy "
-                                   f"restatement of trace_batch in a {cores}-process fork pool "
-                                   f"(phg.py:184-207); host {model}"},
+                         "sample": f"{cpu_sample_note(cfg, len(seeds))} per step, numpy "
+                                   f"restatement of trace_batch (pinned bit-exact to the "
+                                   f"reference) in a persistent {cores}-process fork pool, "
+                                   f"{len(seeds) // cores} seeds per worker (phg.py:184-207 "
+                                   f"slicing); host {model}"},
         "e2e": {"value": v, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
+
+
+def touched_footprint(cfg, off, verts):
+    """How much of the field a trace actually visits (decides whether the gathers are served
+    from L2 or HBM): distinct voxels holding a vertex, and the percentiles of each strand's
+    top z (in voxels).  Computed on the device from the warm-up trace's CSR."""
+    import torch
+
+    from paper_2604_05794_b200 import synth
+
+    n = cfg.n
+    ijk = torch.floor(verts / synth.VOXEL_MM).to(torch.int64).clamp_(0, n - 1)
+    lin = (ijk[:, 0] * n + ijk[:, 1]) * n + ijk[:, 2]
+    plane = torch.zeros(n ** 3, dtype=torch.uint8, device=verts.device)
+    plane[lin] = 1
+    distinct = int(plane.sum(dtype=torch.int64).item())
+    del plane, lin
+    ends = off[1:] - 1
+    z = ijk[ends.clamp(min=0), 2].double()
+    q = torch.quantile(z[torch.randperm(z.numel(), device=z.device)[: 1 << 20]],
+                       torch.tensor([0.5, 0.9, 0.99], dtype=torch.float64, device=z.device))
+    return {"distinct_voxels_with_vertices": distinct,
+            "frac_of_field_voxels": distinct / n ** 3,
+            "vertex_voxel_bytes": distinct * 16,
+            "strand_end_z_vox_p50_p90_p99": [float(v) for v in q.tolist()],
+            "note": "the corner gathers read these voxels and their +1 neighbours (<= 8x); "
+                    "compare with the 126 MB L2"}
+
+
+def roofline_block(cfg, accepted, kernel_ms):
+    """The trace kernel's roofline from its OWN config's ncu capture
+    (profiles/ncu_<cfg>_trace.json; C4 runs C3's kernel on C3's field).  The kernel is bound
+    by instruction issue (its 2x8 corner gathers are served mostly on chip), so the primary
+    fraction is issue-based: warp instructions per step (ncu) x accepted steps / kernel time,
+    against 148 SMs x 4 schedulers x 1 warp-instruction/clock at the max SM clock.  HBM (the
+    SURVEY 8(d) algorithmic 281 B/step and the ncu DRAM bytes), L1 and L2 fractions sit
+    beside it."""
+    name = "C3" if cfg.name == "C4" else cfg.name
+    path = os.path.join(ROOT, "profiles", f"ncu_{name}_trace.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+    except Exception:  # noqa: BLE001
+        d = None
+    peak_hbm, peak_kind = measured_peak()
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            mhz = float(json.load(f).get("sm_max_mhz", 1965.0))
+    except Exception:  # noqa: BLE001
+        mhz = 1965.0
+    sec = kernel_ms / 1e3
+    algo_gbs = accepted * BYTES_PER_STEP / sec / 1e9
+    out = {"bound": "issue", "kernel": "trace_kernel", "kernel_ms": kernel_ms,
+           "unit": "Gwarp-inst/s", "peak": 148 * 4 * mhz * 1e6 / 1e9,
+           "peak_source": f"148 SMs x 4 schedulers x 1 warp-inst/clk x {mhz:.0f} MHz "
+                          "(MEASURED_PEAKS.json sm_max_mhz)",
+           "achieved": None, "frac": None, "traffic": None,
+           "hbm": {"algorithmic_bytes_per_step": BYTES_PER_STEP,
+                   "algorithmic_gbs": algo_gbs, "peak_gbs": peak_hbm,
+                   "peak_source": peak_kind},
+           "source": os.path.relpath(path, ROOT) if d else None}
+    if not d:
+        out["note"] = f"no ncu capture for {name}: issue fraction unavailable"
+        return out
+    m = d.get("metrics", {})
+
+    def num(k):
+        try:
+            return float(m[k][0])
+        except Exception:  # noqa: BLE001
+            return None
+
+    steps_cap = float(d["steps_per_launch"])
+    winst_step = num("smsp__inst_executed.sum") / steps_cap
+    achieved = winst_step * accepted / sec / 1e9
+    traffic = d["dram_bytes_per_launch"] * accepted / steps_cap
+    out.update({"achieved": achieved, "frac": achieved / out["peak"], "traffic": traffic,
+                "warp_inst_per_step": winst_step, "inst_per_step": winst_step * 32})
+    out["hbm"].update({"dram_bytes_per_step": d["dram_bytes_per_step"],
+                       "dram_gbs": traffic / sec / 1e9,
+                       "dram_frac": traffic / sec / 1e9 / peak_hbm})
+    pct = lambda k: (num(k) / 100.0 if num(k) is not None else None)  # noqa: E731
+    out["ncu"] = {"issue_active": pct("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+                  "fp64_pipe": pct("sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active"),
+                  "xu_pipe": pct("sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active"),
+                  "l1_frac": pct("l1tex__throughput.avg.pct_of_peak_sustained_active"),
+                  "l2_frac": pct("lts__throughput.avg.pct_of_peak_sustained_elapsed"),
+                  "dram_frac": pct("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"),
+                  "l1_hit": pct("l1tex__t_sector_hit_rate.pct"),
+                  "l2_hit": pct("lts__t_sector_hit_rate.pct"),
+                  "warps_per_sm": num("sm__warps_active.avg.per_cycle_active"),
+                  "registers": num("launch__registers_per_thread"),
+                  "kernel_ms_under_ncu": num("gpu__time_duration.sum"),
+                  "stalls_per_issue": d.get("stalls_per_issue"),
+                  "gather_gbs": d.get("gather_gbs")}
+    return out
+
+
+def init_dist(args, ws, local):
+    """One process per GPU.  NCCL when every local rank has its own device (the driver's
+    multi-GPU runs); gloo when ranks share a device (--dist-backend auto on a box with fewer
+    GPUs than ranks: exercises the N > 1 code path through the real kernel for correctness,
+    its timings are not a scaling measurement).  Returns (device, collective device, backend,
+    shared)."""
+    import torch
+    import torch.distributed as dist
+
+    ndev = max(torch.cuda.device_count(), 1)
+    lws = int(os.environ.get("LOCAL_WORLD_SIZE", str(ws)))
+    backend = args.dist_backend
+    if backend == "auto":
+        backend = "nccl" if ndev >= lws else "gloo"
+    index = local % ndev
+    torch.cuda.set_device(index)
+    dev = torch.device("cuda", index)
+    if ws > 1:
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
+    coll = dev if backend == "nccl" else torch.device("cpu")
+    return dev, coll, backend, ws > 1 and ndev < lws
 
 
 def run_ours(args):
@@ -256,11 +422,8 @@ def run_ours(args):
     from paper_2604_05794_b200.volume import DeviceField
 
     ws, rank, local = dist_env()
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if ws > 1:
-        dist.init_process_group("nccl", device_id=dev)
-    cfg = synth.CONFIGS[args.config]
+    dev, coll, backend, shared = init_dist(args, ws, local)
+    cfg = synth.CONFIGS[resolve_config(args, ws)]
     # C4 is BASELINE's scaling sweep: 4M global seeds split over the ranks (strong scaling);
     # every other config fixes the seeds per GPU (weak scaling)
     strong = cfg.name == "C4" and not args.seeds
@@ -275,70 +438,107 @@ def run_ours(args):
     if ws == 1 and not args.no_cpu:
         ori_host, occ_host = ori.cpu().numpy(), occ.cpu().numpy()
     all_seeds, all_dirs = synth.config_seeds(cfg, per_rank * ws, ori, occ)
+    cpu_seeds = None
+    if ori_host is not None:  # C1 all seeds, C2-C5 the first 16384
+        k = min(args.cpu_sample or (cfg.seeds if cfg.name == "C1" else CPU_SUBSET), len(all_seeds))
+        cpu_seeds = (np.ascontiguousarray(all_seeds[:k]), np.ascontiguousarray(all_dirs[:k]))
     del ori, occ
     torch.cuda.empty_cache()
 
     s_host = np.ascontiguousarray(all_seeds[rank * per_rank:(rank + 1) * per_rank])
     d_host = np.ascontiguousarray(all_dirs[rank * per_rank:(rank + 1) * per_rank])
+    del all_seeds, all_dirs
     s_dev = torch.from_numpy(s_host).to(dev)
     d_dev = torch.from_numpy(d_host).to(dev)
     stream = torch.cuda.current_stream(dev)
     tracer = phg.Tracer()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
 
-    def step():
+    n_t = torch.tensor([per_rank], dtype=torch.int64, device=dev)
+
+    def step_csr():
         off, verts, ent = phg.trace_device(field, s_dev, d_dev, params, tracer=tracer,
                                            stream=stream)
         if ws > 1:  # the one collective: global CSR placement of this rank's strands
-            pdist.exchange_counts(per_rank, int(verts.shape[0]), device=dev)
+            pdist.exchange_counts(per_rank, int(verts.shape[0]), device=coll)
         return off, verts
 
+    def step():
+        # the device-resident result: strand rows = the reference's buf[i, :keep[i]]
+        # (phg.py:159-162), no host synchronisation inside the step
+        rs = phg.trace_device_rows(field, s_dev, d_dev, params, tracer=tracer, stream=stream)
+        if ws > 1:  # the one collective: (strands, vertices) of every rank -> CSR placement
+            pdist.exchange_counts_device(n_t, rs.counters[1:2], device=coll)
+        return rs
+
     if args.sweep:
-        sweep_variants(args, step, tracer, flush)
+        sweep_variants(args, step_csr, tracer, flush)
         return
     if args.sweep_sizes:
         sweep_launch_sizes(field, s_dev, d_dev, params, tracer, stream,
                            [int(v) for v in args.sweep_sizes.split(",")])
         return
 
+    # warm-up, and the reference's step count from the CSR path (checked against the rows')
     for _ in range(args.warmup):
         flush.zero_()
-        off, verts = step()
+        off, verts = step_csr()
     torch.cuda.synchronize()
-    steps_per_trace = int(verts.shape[0]) - per_rank  # sum(len - 1) over returned strands
-    accepted = tracer.last_steps()
+    my_steps = int(verts.shape[0]) - per_rank  # sum(len - 1) over this rank's strands
+    footprint = touched_footprint(cfg, off, verts) if rank == 0 else None
     del off, verts
+    for _ in range(args.warmup):
+        flush.zero_()
+        rs = step()
+    torch.cuda.synchronize()
+    rows_steps = rs.steps
+    accepted = tracer.last_steps()
+    del rs
+    if rows_steps != my_steps:
+        raise RuntimeError(f"rows path steps {rows_steps} != CSR path steps {my_steps}")
+    # whole-job steps: every rank's own count (ranks trace different seeds)
+    tot = torch.tensor([my_steps], dtype=torch.int64, device=coll)
+    if ws > 1:
+        dist.all_reduce(tot, op=dist.ReduceOp.SUM)
+    total_steps = int(tot.item())
 
-    clocks = ClockSampler(local)
+    def timed(fn, kern):
+        """K steps between CUDA events on the launching stream, barrier + synchronize on
+        both sides; max over ranks."""
+        if ws > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            flush.zero_()
+            r = fn()
+            if kern is not None:
+                kern.append(tracer.last_kernel_ms()[0])
+            del r
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if ws > 1:
+            dist.barrier()
+        t = torch.tensor([e0.elapsed_time(e1) / args.steps], dtype=torch.float64, device=coll)
+        if ws > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    clocks = ClockSampler(dev.index)
     clocks.start()
     kern_ms = []
-    if ws > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(args.steps):
-        flush.zero_()
-        off, verts = step()
-        kern_ms.append(tracer.last_kernel_ms()[0])
-    e1.record(stream)
-    torch.cuda.synchronize()
-    if ws > 1:
-        dist.barrier()
-    ms = e0.elapsed_time(e1) / args.steps
+    ms_max = timed(step, None)  # no host sync inside the timed rows steps
     clk = clocks.stop()
-    t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if ws > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
-    total_steps = steps_per_trace * ws
+    ms_csr = timed(step_csr, kern_ms)  # kernel durations read per step (host sync per step)
     value = total_steps / (ms_max / 1e3)
-    del off, verts
+    value_csr = total_steps / (ms_csr / 1e3)
 
     # e2e: host (pinned) buffers through the C ABI, copies inside the timed region
     e2e = None
     if not args.no_e2e:
-        e2e = e2e_leg(args, tracer, field, params, s_host, d_host, per_rank, ws, dev, steps_per_trace)
+        e2e = e2e_leg(args, tracer, field, params, s_host, d_host, per_rank, ws, coll,
+                      total_steps)
 
     driver = a9 = dropin = None
     if not args.no_driver and ws == 1:
@@ -352,27 +552,10 @@ def run_ours(args):
         dropin = dropin_leg(ori_host, occ_host, s_host, d_host, params)
 
     kernel_ms = float(np.mean(kern_ms))
-    peak, peak_kind = measured_peak()
-    achieved = accepted * BYTES_PER_STEP / (kernel_ms / 1e3) / 1e9
-    traffic, traffic_steps = ncu_traffic()
-    if traffic is not None and traffic_steps:
-        traffic = traffic * accepted / traffic_steps
-
     cpu = None
     if ws == 1 and not args.no_cpu:  # the CPU baseline is an N=1 figure (rank 0 only)
         cores, model = cpu_host_info()
-        sample = args.cpu_sample or max(1024, cores * 256)
-        s_cpu, t_cpu = cpu_numpy_port(ori_host, occ_host, s_host[:sample], d_host[:sample],
-                                      params, cores)
-        c_s, c_t = cpu_c_port(ori_host, occ_host, s_host[: sample * 4], d_host[: sample * 4],
-                              params, cores)
-        cpu = {"value": s_cpu / t_cpu, "unit": "steps/s", "cores": cores, "kind": "port",
-               "sample": f"first {min(sample, per_rank)} seeds of {cfg.name} (numpy restatement "
-                         f"of trace_batch, {cores}-process fork pool like phg.py:184-207); "
-                         f"host {model}",
-               "c_port_value": c_s / c_t,
-               "c_port_sample": f"first {min(sample * 4, per_rank)} seeds, C oracle, "
-                                f"{cores} OpenMP threads"}
+        cpu = cpu_legs(cfg, ori_host, occ_host, cpu_seeds[0], cpu_seeds[1], cores, model)
 
     if rank == 0:
         line = {
@@ -385,24 +568,22 @@ def run_ours(args):
                        "seeds_per_gpu": per_rank, "global_seeds": per_rank * ws,
                        "max_vertices": params.max_vertices, "step_mm": params.step_mm,
                        "batch_size": per_rank * ws, "parallelism": f"seed-partition x{ws}",
-                       "l2": f"256 MiB flush write between timed steps; packed field "
-                             f"{(cfg.n + 2) ** 3 * 16 / 2 ** 30:.1f} GiB > L2"},
-            "steps_per_trace": steps_per_trace, "accepted_steps_per_trace": accepted,
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "trace_kernel", "kernel_ms": kernel_ms,
-                         "bytes_per_step": BYTES_PER_STEP, "peak_source": peak_kind,
-                         "dram_frac": (traffic / (kernel_ms / 1e3) / 1e9 / peak
-                                       if traffic is not None else None),
-                         "note": "achieved counts the algorithmic 281 B/step (SURVEY 8(d)); the "
-                                 "2x8 corner gathers are served by L1/L2 (traffic = ncu DRAM "
-                                 "bytes, ~25 B/step), so frac may exceed 1 and the kernel is "
-                                 "bound by issue/fp64/XU latency (binding), not by HBM",
-                         "binding": binding_resource()},
+                       "dist_backend": backend if ws > 1 else None,
+                       "ranks_share_gpu": shared,
+                       "l2": "256 MiB flush write between timed steps",
+                       "field_bytes": (cfg.n + 2) ** 3 * 16, "touched_footprint": footprint},
+            "steps_per_trace": total_steps, "accepted_steps_per_trace": accepted,
+            "output": "device-resident strand rows (phg_trace_rows: the reference's buf[i, "
+                      ":keep[i]], phg.py:159-162); value_csr adds the CSR scan + gather (K2)",
+            "value_csr": value_csr, "ms_per_step_csr": ms_csr,
+            "roofline": roofline_block(cfg, accepted, kernel_ms),
             "cpu_baseline": cpu, "e2e": e2e, "clocks": clk, "driver": driver, "a9": a9,
             "dropin": dropin,
-            "gpu_launches": args.steps * phg.LAUNCHES_PER_TRACE,
+            "gpu_launches": args.steps * phg.LAUNCHES_PER_TRACE_ROWS,
         }
+        if shared:
+            line["note"] = ("ranks share one GPU (gloo): validates the N > 1 code path through "
+                            "the real kernel; not a scaling measurement")
         print(json.dumps(line), flush=True)
     if ws > 1:
         dist.destroy_process_group()
@@ -584,13 +765,13 @@ def sweep_variants(args, step, tracer, flush):
     os.environ.pop("PHG_VARIANT", None)
 
 
-def e2e_leg(args, tracer, field, params, s_host, d_host, per_rank, ws, dev, steps_per_trace):
+def e2e_leg(args, tracer, field, params, s_host, d_host, per_rank, ws, coll, total_steps):
     """Seeds from pinned host memory in, full CSR (offsets, entered, verts) out to pinned host."""
     import torch
     import torch.distributed as dist
 
     n = per_rank
-    stream = torch.cuda.current_stream(dev)
+    stream = torch.cuda.current_stream()
     err = None
     try:  # every rank pins ~24 B x its output vertices; agree on success before any collective
         pin_s = torch.from_numpy(s_host).pin_memory()
@@ -603,7 +784,7 @@ def e2e_leg(args, tracer, field, params, s_host, d_host, per_rank, ws, dev, step
     except (RuntimeError, MemoryError) as exc:
         err = str(exc).splitlines()[0][:200] if str(exc) else type(exc).__name__
     if ws > 1:
-        ok = torch.tensor([0 if err else 1], dtype=torch.int32, device=dev)
+        ok = torch.tensor([0 if err else 1], dtype=torch.int32, device=coll)
         dist.all_reduce(ok, op=dist.ReduceOp.MIN)
         if not ok.item() and err is None:
             err = "another rank could not allocate its pinned host buffers"
@@ -626,12 +807,12 @@ def e2e_leg(args, tracer, field, params, s_host, d_host, per_rank, ws, dev, step
         total = one()
     torch.cuda.synchronize()
     dt = (time.perf_counter() - t0) / args.steps
-    tt = torch.tensor([dt], dtype=torch.float64, device=dev)
+    tt = torch.tensor([dt], dtype=torch.float64, device=coll)
     if ws > 1:
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
     dt = float(tt.item())
     # the PCIe floor of this leg: a plain pinned D2H of the same payload size
-    probe = torch.empty(min(total * 24, 2 << 30), dtype=torch.uint8, device=dev)
+    probe = torch.empty(min(total * 24, 2 << 30), dtype=torch.uint8, device="cuda")
     host = torch.empty(probe.numel(), dtype=torch.uint8).pin_memory()
     host.copy_(probe, non_blocking=True)
     torch.cuda.synchronize()
@@ -642,7 +823,7 @@ def e2e_leg(args, tracer, field, params, s_host, d_host, per_rank, ws, dev, step
     d2h_gbs = 3 * probe.numel() / (time.perf_counter() - t0) / 1e9
     del probe, host
     floor_ms = (total * 24 + (n + 1) * 8 + n) / d2h_gbs / 1e6
-    return {"value": steps_per_trace * ws / dt, "unit": "steps/s",
+    return {"value": total_steps / dt, "unit": "steps/s",
             "pcie_d2h_gbs": d2h_gbs, "pcie_floor_ms": floor_ms,
             "frac_of_pcie_floor": floor_ms / (dt * 1e3), "chunk": args.e2e_chunk,
             "h2d_bytes_per_step": int(2 * n * 24), "d2h_bytes_per_step": int((n + 1) * 8 + n +

@@ -95,6 +95,32 @@ phg_status phg_trace(phg_ctx* c, const phg_field* f, const phg_params_v1* p,
  * (n_verts,3) float64 CSR payload.  verts_cap is in vertices. Blocks when verts is host memory. */
 phg_status phg_gather(phg_ctx* c, double* verts, int64_t verts_cap, void* stream);
 
+/* Device-resident strand rows: the reference's own trace buffer `buf` (N, max_vertices, 3)
+ * (phg.py:85) with its per-seed `keep` (phg.py:159-161), i.e. strand i's vertices are
+ *   rows[row(i) * row_stride .. + 3 * lengths[i]]   (f64 x,y,z; row(i) = rowmap ? rowmap[i] : i)
+ * which is exactly buf[i, :keep] -- the array trace_batch returns for seed i, without the
+ * per-strand copy into a list (phg.py:162) or our CSR gather.  Every pointer is device memory
+ * owned by the context and valid until the next trace on it. */
+typedef struct {
+    const double* rows;        /* strand rows, row_stride doubles apart */
+    const int32_t* rowmap;     /* (n) row of seed i, or NULL: row i */
+    const int64_t* lengths;    /* (n) kept vertex count of seed i (len(vertices_i)) */
+    const uint8_t* entered;    /* (n) entered flag of seed i */
+    int64_t row_stride;        /* doubles per row: max_vertices rounded up to 4, times 3 */
+    int64_t n;                 /* seeds */
+    const uint64_t* counters;  /* device: [0] accepted steps (vertices appended before the
+                                  trailing-coast trim), [1] sum of lengths (kept vertices) */
+} phg_rows_v1;
+
+/* Trace n seeds into device-resident strand rows (relaxed mode, phg_field's cap plane as in
+ * phg_trace).  Asynchronous: enqueues the locality sort and the trace kernel on `stream` and
+ * returns without waiting; `out` is filled at once, its contents are ready when the stream
+ * reaches them.  Seeds may be host or device memory (host seeds are staged synchronously).
+ * The sum of lengths minus n is the reference's step count sum(len(vertices) - 1). */
+phg_status phg_trace_rows(phg_ctx* c, const phg_field* f, const phg_params_v1* p,
+                          const double* seed_pos, const double* seed_dir, int64_t n,
+                          phg_rows_v1* out, void* stream);
+
 /* End-to-end variant of phg_trace + phg_gather for HOST seeds and HOST outputs: seeds are
  * traced in chunks of `chunk` (<= 0: n/4, at least 65536) and the D2H copy of chunk k's
  * vertices (on an internal copy stream) overlaps the device work of chunk k+1.  offsets
@@ -107,8 +133,9 @@ phg_status phg_trace_to_host(phg_ctx* c, const phg_field* f, const phg_params_v1
                              int64_t chunk, int64_t* offsets, uint8_t* entered, double* verts,
                              int64_t verts_cap, int64_t* n_verts_out, void* stream);
 
-/* Per-strand raw counters of the last trace (diagnostics / step accounting):
- * steps (n) int64 = integration steps each strand accepted (vertices appended). */
+/* Accepted integration steps of the last phg_trace, phg_trace_rows (waits for its stream) or
+ * phg_trace_to_host call on the context:
+ * one total over all strands (sum of vertices appended, before the trailing-coast trim). */
 phg_status phg_last_steps(phg_ctx* c, int64_t* total_steps);
 
 /* ---- device batch driver (replaces init_guide_strands, phg.py:210-260, with

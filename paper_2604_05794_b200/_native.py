@@ -29,7 +29,7 @@ EXPORTS = (
     "phg_grow_fetch",
     "phg_trace_to_host", "phg_stnd_encode", "phg_field_from_oovl", "phg_link", "phg_link_fetch",
     "phg_grow_begin", "phg_grow_scalp_batch", "phg_grow_field_begin", "phg_grow_field_batch",
-    "phg_grow_commits", "phg_grow_apply", "phg_grow_end",
+    "phg_grow_commits", "phg_grow_apply", "phg_grow_end", "phg_trace_rows",
 )
 
 
@@ -57,6 +57,15 @@ class Params(ctypes.Structure):
     ]
 
 
+class Rows(ctypes.Structure):
+    """phg_rows_v1: device-resident strand rows of the last phg_trace_rows"""
+
+    _fields_ = [("rows", ctypes.c_void_p), ("rowmap", ctypes.c_void_p),
+                ("lengths", ctypes.c_void_p), ("entered", ctypes.c_void_p),
+                ("row_stride", ctypes.c_int64), ("n", ctypes.c_int64),
+                ("counters", ctypes.c_void_p)]
+
+
 _lib = None
 _load_error = None
 
@@ -78,6 +87,8 @@ def _declare(lib):
         "phg_trace": (S, [VP, VP, ctypes.POINTER(Params), VP, VP, I64, VP, VP, VP,
                           ctypes.POINTER(I64), VP]),
         "phg_gather": (S, [VP, VP, I64, VP]),
+        "phg_trace_rows": (S, [VP, VP, ctypes.POINTER(Params), VP, VP, I64,
+                               ctypes.POINTER(Rows), VP]),
         "phg_trace_to_host": (S, [VP, VP, ctypes.POINTER(Params), VP, VP, I64, I64, VP, VP, VP,
                                   I64, ctypes.POINTER(I64), VP]),
         "phg_last_steps": (S, [VP, ctypes.POINTER(I64)]),

@@ -11,7 +11,8 @@ single-GPU CSR byte for byte -- the analogue of the reference's
 
 The only communication is one all-gather of per-rank (strands, vertices)
 counts, from which every rank derives its global CSR offsets; payloads stay
-rank-local unless ``gather_to_root`` is asked for.  The same code runs over
+rank-local unless ``gather_to_root`` is asked for, which moves each rank's payload
+to the root only (point-to-point), never to every rank.  The same code runs over
 NCCL (CUDA tensors) and gloo (CPU tensors, used by the CPU tests).
 """
 
@@ -56,6 +57,21 @@ def exchange_counts(n_strands: int, n_verts: int, group=None, device="cpu") -> S
                      int(counts[:, 0].sum()), int(counts[:, 1].sum()))
 
 
+def exchange_counts_device(n_strands_t, n_verts_t, group=None, device="cpu"):
+    """exchange_counts without a host synchronisation (NCCL): the (strands, vertices) pair is
+    built from device tensors (e.g. phg_trace_rows' kept-vertex counter) and all-gathered on
+    the stream; returns the (world, 2) tensor of every rank's counts, in rank order."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    mine = torch.cat([n_strands_t.reshape(1), n_verts_t.reshape(1)]).to(device=device,
+                                                                        dtype=torch.int64)
+    allc = [torch.empty_like(mine) for _ in range(world)]
+    dist.all_gather(allc, mine, group=group)
+    return torch.stack(allc)
+
+
 def trace_sharded(trace_fn, seed_pos, seed_dir, group=None, device="cpu"):
     """Trace this rank's slice of a batch and return it with global CSR placement.
 
@@ -91,6 +107,41 @@ def _allgather_v(t, group=None):
     outs = [torch.empty_like(pad) for _ in range(world)]
     dist.all_gather(outs, pad, group=group)
     return [o[:s] for o, s in zip(outs, sizes)]
+
+
+def _gather_v_to_root(t, group=None, root=0):
+    """Gather 1-D tensors of different lengths on ``root`` (rank order) with point-to-point
+    sends: only the lengths are all-gathered, and each payload crosses the fabric once, to
+    root (NCCL on CUDA tensors, gloo on CPU tensors).  Returns the list on root, None
+    elsewhere."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    t = t.contiguous()
+    n = torch.tensor([t.numel()], dtype=torch.int64, device=t.device)
+    ns = [torch.empty_like(n) for _ in range(world)]
+    dist.all_gather(ns, n, group=group)
+    sizes = [int(x.item()) for x in ns]
+
+    def glob(r):
+        return dist.get_global_rank(group, r) if group is not None else r
+
+    if rank != root:
+        if t.numel():
+            dist.send(t, dst=glob(root), group=group)
+        return None
+    out = []
+    for r in range(world):
+        if r == root:
+            out.append(t)
+            continue
+        buf = torch.empty(sizes[r], dtype=t.dtype, device=t.device)
+        if sizes[r]:
+            dist.recv(buf, src=glob(r), group=group)
+        out.append(buf)
+    return out
 
 
 def init_guide_strands_multirank(seeds, normals, counts, params, backend, group=None,
@@ -150,10 +201,11 @@ def init_guide_strands_multirank(seeds, normals, counts, params, backend, group=
     logs = _allgather_v(torch.tensor(log, dtype=torch.int64, device=device), group)
     nev = torch.tensor([never], dtype=torch.int64, device=device)
     dist.all_reduce(nev, group=group)
+    # the segment payloads travel to rank 0 only (the one rank that assembles the result)
     lens = torch.as_tensor(np.diff(offsets), dtype=torch.int64, device=device)
-    all_lens = _allgather_v(lens, group)
-    all_verts = _allgather_v(torch.as_tensor(verts.reshape(-1), device=device), group)
-    all_root = _allgather_v(torch.as_tensor(rooted.astype(np.uint8), device=device), group)
+    all_lens = _gather_v_to_root(lens, group)
+    all_verts = _gather_v_to_root(torch.as_tensor(verts.reshape(-1), device=device), group)
+    all_root = _gather_v_to_root(torch.as_tensor(rooted.astype(np.uint8), device=device), group)
     if rank != 0:
         return None
     per_rank = []
@@ -192,40 +244,46 @@ def init_guide_strands_multirank(seeds, normals, counts, params, backend, group=
 
 def gather_to_root(offsets_global, verts, entered, info: ShardInfo, group=None, device="cpu",
                    root=0):
-    """Concatenate every rank's CSR on ``root`` (pad-to-max all-gather; NCCL has no gatherv).
+    """Concatenate every rank's CSR on ``root``: each rank sends its payload straight to root
+    (point-to-point; sizes are already known from ``exchange_counts``), so no rank receives
+    any other rank's vertices except root.
 
     Returns (offsets (N+1,), verts (M,3), entered (N,)) as numpy on root, None elsewhere.
     """
     import torch
     import torch.distributed as dist
 
-    mx_s = int(info.counts[:, 0].max())
-    mx_v = int(info.counts[:, 1].max())
+    def as_t(a, dtype):
+        t = a if torch.is_tensor(a) else torch.as_tensor(np.asarray(a))
+        return t.to(device=device, dtype=dtype).contiguous()
+
     k = int(info.counts[info.rank, 0])
-    m = int(info.counts[info.rank, 1])
-    v = torch.zeros((max(mx_v, 1), 3), dtype=torch.float64, device=device)
-    e = torch.zeros(max(mx_s, 1), dtype=torch.uint8, device=device)
-    o = torch.zeros(max(mx_s, 1), dtype=torch.int64, device=device)
-    v[:m] = torch.as_tensor(np.asarray(verts) if not torch.is_tensor(verts) else verts,
-                            dtype=torch.float64, device=device).reshape(-1, 3)
-    e[:k] = torch.as_tensor(np.asarray(entered) if not torch.is_tensor(entered) else entered,
-                            device=device).to(torch.uint8)
-    og = offsets_global if torch.is_tensor(offsets_global) else torch.as_tensor(
-        np.asarray(offsets_global))
-    o[:k] = og[:k].to(device=device, dtype=torch.int64)
-    vs = [torch.empty_like(v) for _ in range(info.world)]
-    es = [torch.empty_like(e) for _ in range(info.world)]
-    os_ = [torch.empty_like(o) for _ in range(info.world)]
-    dist.all_gather(vs, v, group=group)
-    dist.all_gather(es, e, group=group)
-    dist.all_gather(os_, o, group=group)
+    v = as_t(verts, torch.float64).reshape(-1)
+    e = as_t(entered, torch.uint8).reshape(-1)[:k]
+    o = as_t(offsets_global, torch.int64).reshape(-1)[:k]
+
+    def glob(r):
+        return dist.get_global_rank(group, r) if group is not None else r
+
     if info.rank != root:
+        for t in (v, e, o):
+            if t.numel():
+                dist.send(t, dst=glob(root), group=group)
         return None
     parts_v, parts_e, parts_o = [], [], []
     for r in range(info.world):
         kr, mr = int(info.counts[r, 0]), int(info.counts[r, 1])
-        parts_v.append(vs[r][:mr].cpu().numpy())
-        parts_e.append(es[r][:kr].cpu().numpy().astype(bool))
-        parts_o.append(os_[r][:kr].cpu().numpy())
+        if r == root:
+            bufs = (v, e, o)
+        else:
+            bufs = (torch.empty(3 * mr, dtype=torch.float64, device=device),
+                    torch.empty(kr, dtype=torch.uint8, device=device),
+                    torch.empty(kr, dtype=torch.int64, device=device))
+            for t in bufs:
+                if t.numel():
+                    dist.recv(t, src=glob(r), group=group)
+        parts_v.append(bufs[0].cpu().numpy().reshape(-1, 3))
+        parts_e.append(bufs[1].cpu().numpy().astype(bool))
+        parts_o.append(bufs[2].cpu().numpy())
     offsets = np.concatenate(parts_o + [np.array([info.n_verts], np.int64)])
     return offsets, np.concatenate(parts_v), np.concatenate(parts_e)

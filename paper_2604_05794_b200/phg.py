@@ -104,6 +104,15 @@ class Tracer:
                       "phg_trace_to_host")
         return int(total.value)
 
+    def trace_rows(self, field, params, seed_pos, seed_dir, n, stream=0):
+        """phg_trace_rows: asynchronous trace into device-resident strand rows."""
+        p = _native.params_struct(params)
+        out = _native.Rows()
+        _native.check(self._lib.phg_trace_rows(self.handle, field.handle, ctypes.byref(p),
+                                               seed_pos, seed_dir, n, ctypes.byref(out), stream),
+                      "phg_trace_rows")
+        return out
+
     def gather(self, verts_ptr, cap, stream=0):
         _native.check(self._lib.phg_gather(self.handle, verts_ptr, cap, stream), "phg_gather")
 
@@ -130,6 +139,8 @@ class Tracer:
 # morton keys, CUB radix sort (histogram, exclusive-sum, 4 onesweep passes), trace,
 # CUB scan (init + scan), gather -- as listed by ncu (profiles/r01_v0_launches.csv).
 LAUNCHES_PER_TRACE = 11
+# phg_trace_rows: morton keys, the 6 CUB radix-sort launches, trace (no scan, no gather)
+LAUNCHES_PER_TRACE_ROWS = 8
 
 _TRACER = None
 
@@ -268,6 +279,96 @@ def trace_device(field, seed_pos, seed_dir, params, tracer=None, stream=None, or
     if total:
         tr.gather(verts.data_ptr(), total, st.cuda_stream)
     return offsets, verts, entered
+
+
+class _CudaArray:
+    """Zero-copy __cuda_array_interface__ view of library-owned device memory."""
+
+    def __init__(self, ptr, shape, typestr):
+        # no "stream": the producer is the caller's own stream (RowSet's contract)
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr,
+                                         "data": (int(ptr or 0), True), "version": 3,
+                                         "strides": None}
+
+
+class RowSet:
+    """Device-resident result of ``trace_device_rows``: the reference's own trace buffer
+    ``buf`` (phg.py:85) and ``keep`` (phg.py:159-161) -- strand i is ``strand(i)`` =
+    buf[i, :keep[i]], the array trace_batch returns for seed i.  Views of the tracer's
+    memory, valid until its next trace.  ``steps`` (the reference's sum(len - 1)) and
+    ``kept`` synchronise on first use; everything else stays asynchronous."""
+
+    def __init__(self, tracer, raw, device, stream):
+        import torch
+
+        self._tracer, self.n, self.row_stride = tracer, int(raw.n), int(raw.row_stride)
+        self.stream = stream  # the rows are produced on this stream
+        n = self.n
+        nrows = n
+        with torch.cuda.device(device):
+            def view(ptr, shape, ts):
+                if not ptr or not all(shape):
+                    return torch.empty(shape, dtype={"<f8": torch.float64, "<i4": torch.int32,
+                                                     "<i8": torch.int64, "|u1": torch.uint8}[ts],
+                                       device=device)
+                return torch.as_tensor(_CudaArray(ptr, shape, ts), device=device)
+
+            self.rows = view(raw.rows, (nrows, self.row_stride), "<f8")
+            self.rowmap = view(raw.rowmap, (n,), "<i4") if raw.rowmap else None
+            self.lengths = view(raw.lengths, (n,), "<i8")
+            self.entered = view(raw.entered, (n,), "|u1")
+            self.counters = view(raw.counters, (2,), "<i8")  # u64 counters, < 2^63
+        self._kept = None
+
+    def row_of(self, i):
+        return int(self.rowmap[i]) if self.rowmap is not None else int(i)
+
+    def strand(self, i):
+        """(len_i, 3) f64 device view of seed i's vertices."""
+        k = int(self.lengths[i])
+        return self.rows[self.row_of(i), : 3 * k].view(k, 3)
+
+    @property
+    def kept(self):
+        if self._kept is None:
+            self._kept = int(self.counters[1].item())
+        return self._kept
+
+    @property
+    def steps(self):
+        """sum over strands of (len(vertices) - 1): the reference's step count."""
+        return self.kept - self.n
+
+    def to_csr(self):
+        """(offsets (n+1,), verts (M,3), entered (n,)) torch CUDA tensors, built with torch
+        ops from the rows (validation / convenience; the library's CSR path is
+        trace_device)."""
+        import torch
+
+        off = torch.zeros(self.n + 1, dtype=torch.int64, device=self.rows.device)
+        torch.cumsum(self.lengths, 0, out=off[1:])
+        rows = (self.rowmap.long() if self.rowmap is not None
+                else torch.arange(self.n, device=self.rows.device))
+        seg = torch.repeat_interleave(torch.arange(self.n, device=self.rows.device),
+                                      self.lengths)
+        j = torch.arange(int(off[-1]), device=self.rows.device) - off[seg]
+        r3 = self.rows.view(self.rows.shape[0], -1, 3)
+        return off, r3[rows[seg], j], self.entered
+
+
+def trace_device_rows(field, seed_pos, seed_dir, params, tracer=None, stream=None):
+    """Device API without the CSR copy: torch CUDA seeds in, a ``RowSet`` of device-resident
+    strand rows out (phg_trace_rows), enqueued on ``stream`` without a host synchronisation.
+    Strand i is the reference's buf[i, :keep[i]] (phg.py:159-162)."""
+    import torch
+
+    tr = tracer or _tracer()
+    n = int(seed_pos.shape[0])
+    dev = seed_pos.device
+    st = stream if stream is not None else torch.cuda.current_stream(dev)
+    raw = tr.trace_rows(field, params, seed_pos.data_ptr() if n else None,
+                        seed_dir.data_ptr() if n else None, n, st.cuda_stream)
+    return RowSet(tr, raw, dev, st)
 
 
 # ----------------------------------------------------------------------------------

@@ -163,7 +163,12 @@ def config_seeds(cfg: "Config", count: int, ori=None, occ=None):
     si, di = interior_seeds_torch(occ, ori, ni, cfg.key + 1)
     pos = np.concatenate([sd, si, si])
     dirs = np.concatenate([dd, di, -di])
-    return pos, dirs
+    # interleave the three groups in proportion (disk, disk, +d, -d, ...): every contiguous
+    # slice -- a rank's share, the CPU legs' first-16384 sample -- carries the config's mix
+    grp = [np.arange(nd), nd + np.arange(ni), nd + ni + np.arange(ni)]
+    key = np.concatenate([(g - g[0] + 0.5) / len(g) for g in grp if len(g)])
+    perm = np.argsort(key, kind="stable")
+    return pos[perm], dirs[perm]
 
 
 def interior_seeds(occ: np.ndarray, ori: np.ndarray, count: int, key: int):

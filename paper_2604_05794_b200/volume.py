@@ -15,6 +15,10 @@ from the deferred-commit batch loop (phg.py:229-251) upload the field once.
 from __future__ import annotations
 
 import ctypes
+import hashlib
+import os
+import weakref
+from collections import OrderedDict
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -63,15 +67,29 @@ def _is_torch(a):
     return type(a).__module__.startswith("torch")
 
 
+# Buffers up to this size are hashed in full on every lookup; larger ones are probed at
+# _PROBE_POINTS strided elements (PHG_FIELD_VERIFY=full hashes every buffer in full).
+_FULL_HASH_BYTES = 16 << 20
+_PROBE_POINTS = 1 << 16
+
+
 def _fingerprint(a):
-    """Cheap content probe: a strided sample of the buffer (detects in-place refills)."""
+    """Content probe of a field buffer: a full BLAKE2 hash of small buffers (or of every buffer
+    with PHG_FIELD_VERIFY=full), else a hash of 65536 strided elements plus the last one."""
     if _is_torch(a):
-        flat = a.reshape(-1)
-        step = max(1, flat.numel() // 4096)
-        return hash(flat[::step].cpu().numpy().tobytes())
-    flat = a.reshape(-1)
-    step = max(1, flat.size // 4096)
-    return hash(flat[::step].tobytes())
+        a = a.detach()
+        if a.is_cuda:  # device buffers are probed on the device, then only the sample moves
+            flat = a.reshape(-1)
+            step = max(1, flat.numel() // _PROBE_POINTS)
+            return hash(flat[::step].cpu().numpy().tobytes()) ^ hash(
+                flat[-1:].cpu().numpy().tobytes())
+        a = a.numpy()
+    flat = np.ascontiguousarray(a).reshape(-1)
+    full = os.environ.get("PHG_FIELD_VERIFY", "") == "full"
+    if full or flat.nbytes <= _FULL_HASH_BYTES:
+        return hashlib.blake2b(flat.view(np.uint8), digest_size=16).digest()
+    step = max(1, flat.size // _PROBE_POINTS)
+    return hash(flat[::step].tobytes()) ^ hash(flat[-1:].tobytes())
 
 
 class DeviceField:
@@ -168,35 +186,61 @@ class DeviceField:
         self._near_key = key
 
 
-_CACHE: dict = {}
+# id(vol) -> (key, DeviceField, strong ref or None, finalizer or None).  The entry of a weak-referenceable
+# volume dies with it (weakref.finalize), so neither the ~2 GiB packed field nor a recycled
+# id can outlive the volume; volumes that cannot be weakly referenced are held strongly in an
+# LRU of _STRONG_MAX entries instead.
+_CACHE: "OrderedDict[int, tuple]" = OrderedDict()
+_STRONG_MAX = 2
+
+
+def _drop(vid):
+    hit = _CACHE.pop(vid, None)
+    if hit is not None:
+        hit[1].close()
 
 
 def field_for(vol, stream=0) -> DeviceField:
-    """Device field for ``vol`` (cached on identity, buffers, geometry and a content probe)."""
+    """Device field for ``vol``, cached while ``vol`` lives.
+
+    The cache key covers the volume's identity, its occ/ori buffers (address, shape),
+    geometry and a content probe (_fingerprint): a full hash of buffers up to 16 MiB, a
+    65536-point strided probe of larger ones (PHG_FIELD_VERIFY=full hashes everything).  An
+    in-place edit of a large buffer that the probe misses is not detected: call
+    ``invalidate(vol)`` after editing a volume's occ/ori in place.
+    """
     key = (id(vol), _ptr(vol.occ) if not _is_torch(vol.occ) else vol.occ.data_ptr(),
            _ptr(vol.ori) if not _is_torch(vol.ori) else vol.ori.data_ptr(),
            tuple(vol.occ.shape), tuple(np.asarray(vol.origin, dtype=np.float64).tolist()),
            float(vol.voxel_size), _fingerprint(vol.occ), _fingerprint(vol.ori))
-    hit = _CACHE.get(id(vol))
+    vid = id(vol)
+    hit = _CACHE.get(vid)
     if hit is not None and hit[0] == key:
+        _CACHE.move_to_end(vid)
         return hit[1]
-    if hit is not None:
-        hit[1].close()
+    fin = hit[3] if hit is not None else None  # the same live volume: keep its finalizer
+    _drop(vid)
     f = DeviceField(vol.origin, vol.voxel_size, vol.occ, vol.ori, stream)
-    _CACHE[id(vol)] = (key, f)
+    strong = None
+    if fin is None or not fin.alive:
+        try:
+            fin = weakref.finalize(vol, _drop, vid)
+            fin.atexit = False  # no device frees during interpreter shutdown
+        except TypeError:  # not weak-referenceable: hold it, bounded LRU
+            fin, strong = None, vol
+            while sum(1 for e in _CACHE.values() if e[2] is not None) >= _STRONG_MAX:
+                _drop(next(k for k, e in _CACHE.items() if e[2] is not None))
+    _CACHE[vid] = (key, f, strong, fin)
     return f
 
 
 def invalidate(vol=None):
     """Drop cached device fields (all, or the one of ``vol``)."""
     if vol is None:
-        for _, f in _CACHE.values():
-            f.close()
-        _CACHE.clear()
+        for vid in list(_CACHE):
+            _drop(vid)
     else:
-        hit = _CACHE.pop(id(vol), None)
-        if hit:
-            hit[1].close()
+        _drop(id(vol))
 
 
 def sample_orientation_batch(vol, pts, prev_dirs):

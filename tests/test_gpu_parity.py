@@ -517,3 +517,37 @@ def test_c5_full_size_properties(gpu, oracle_c):
         got = verts[off_h[i]:off_h[i + 1]].cpu().numpy()
         assert np.array_equal(got, v_o[off_o[k]:off_o[k + 1]]), i
         assert bool(ent_h[i]) == bool(ent_o[k])
+
+
+@pytest.mark.parametrize("count,cap", [(3_000, False), (9_000, False), (9_000, True)])
+def test_rows_api_equals_csr_and_oracle(gpu, oracle_c, count, cap):
+    """phg_trace_rows (device-resident strand rows, no CSR copy) holds exactly the strands of
+    the CSR path and of the oracle: strand(i) == buf[i, :keep[i]] (phg.py:159-162), with and
+    without the queue-order row map (n >= 4096 sorts the seeds) and a cap plane."""
+    torch = gpu.torch
+    vol, s, d, p = _config_case("sparse", 64, count, 31, interior=count // 4)
+    at_cap = None
+    if cap:
+        rng = np.random.default_rng(5)
+        at_cap = rng.random(vol.occ.shape) < 0.02
+    off, v, ent = gpu.phg.trace_batch_csr(vol, s, d, p, at_cap=at_cap)
+    f = gpu.volume.field_for(vol)
+    f.set_cap(at_cap)
+    f.set_near(None)
+    tr = gpu.phg.Tracer()
+    rs = gpu.phg.trace_device_rows(f, torch.from_numpy(s).cuda(), torch.from_numpy(d).cuda(),
+                                   p, tracer=tr)
+    assert (rs.rowmap is not None) == (len(s) >= 4096)
+    o2, v2, e2 = rs.to_csr()
+    torch.cuda.synchronize()
+    assert np.array_equal(o2.cpu().numpy(), off)
+    assert np.array_equal(v2.cpu().numpy(), v)
+    assert np.array_equal(e2.cpu().numpy().astype(bool), ent)
+    assert rs.steps == len(v) - len(s) and rs.kept == len(v)
+    i = len(s) // 3
+    assert np.array_equal(rs.strand(i).cpu().numpy(), v[off[i]:off[i + 1]])
+    slab, keep, _ = oracle_c.trace(vol.origin, vol.voxel_size, vol.occ, vol.ori, s, d, p,
+                                   at_cap=at_cap)
+    off_o, v_o = oracle_c.to_csr(slab, keep)
+    assert np.array_equal(off_o, off) and np.array_equal(v_o, v)
+    assert tr.last_steps() >= rs.steps  # accepted steps include trimmed trailing coasts

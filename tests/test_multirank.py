@@ -77,3 +77,33 @@ def test_slice_bounds_match_reference_pool_split():
 
     for n, w in ((10, 3), (1_000_000, 8), (7, 8), (0, 2)):
         assert np.array_equal(slice_bounds(n, w), np.linspace(0, n, w + 1).astype(int))
+
+
+def _counts_worker(rank, world, port, out_path):
+    import sys
+
+    sys.path.insert(0, ROOT)
+    import torch
+    import torch.distributed as dist
+
+    from paper_2604_05794_b200 import dist as pdist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        allc = pdist.exchange_counts_device(torch.tensor([10 + rank]),
+                                            torch.tensor([100 * (rank + 1)]))
+        info = pdist.exchange_counts(10 + rank, 100 * (rank + 1))
+        if rank == 0:
+            np.savez(out_path, dev=allc.numpy(), host=info.counts)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_device_count_exchange_matches_host_exchange(tmp_path):
+    out = str(tmp_path / "c.npz")
+    mp.start_processes(_counts_worker, args=(2, _free_port(), out), nprocs=2, join=True,
+                       start_method="spawn")
+    got = np.load(out)
+    assert np.array_equal(got["dev"], [[10, 100], [11, 200]])
+    assert np.array_equal(got["dev"], got["host"])
