@@ -287,7 +287,7 @@ class _CudaArray:
     def __init__(self, ptr, shape, typestr):
         # no "stream": the producer is the caller's own stream (RowSet's contract)
         self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr,
-                                         "data": (int(ptr or 0), True), "version": 3,
+                                         "data": (int(ptr or 0), False), "version": 3,
                                          "strides": None}
 
 
