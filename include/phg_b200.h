@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define PHG_ABI_VERSION 1
+#define PHG_ABI_VERSION 2 /* 2: phg_params_v1.max_turn_cos, phg_trace_rows */
 
 typedef enum {
     PHG_OK = 0,
@@ -55,11 +55,16 @@ typedef struct {
     int32_t probe_steps;  /* PhgParams.probe_steps */
     int32_t coast_steps;  /* PhgParams.coast_steps */
     uint32_t flags;       /* PHG_FLAG_* */
+    double max_turn_cos;  /* with PHG_FLAG_TURN_STOP: cos of the largest turn a step may make */
 } phg_params_v1;
 
 #define PHG_FLAG_STRICT 0x1u   /* PhgParams.strict: lockstep per-step commits to live_counts */
 #define PHG_FLAG_NO_ORDER 0x2u /* disable the locality (Morton) seed ordering; output order is
                                   seed order either way */
+#define PHG_FLAG_TURN_STOP 0x4u /* opt-in angle stop, NOT in the reference (whose stop tests are
+                                   phg.py:119-142): a step whose direction d' has
+                                   dot(d, d') < max_turn_cos against the previous step direction d
+                                   ends the strand before appending, like the bounds test */
 
 /* ---- field (replaces the OOVolume arrays read by volume.py:205-212) ---------- */
 
@@ -132,6 +137,16 @@ phg_status phg_trace_to_host(phg_ctx* c, const phg_field* f, const phg_params_v1
                              const double* seed_pos, const double* seed_dir, int64_t n,
                              int64_t chunk, int64_t* offsets, uint8_t* entered, double* verts,
                              int64_t verts_cap, int64_t* n_verts_out, void* stream);
+
+/* Checked build only (libphg_b200_checked.so, compiled with PHG_CHECKED; the stand-in for
+ * compute-sanitizer): waits for the device, then reports device-side index-check violations
+ * of the hot kernels (with the first failing check's site id) and the number of live library
+ * buffers whose canary guards (4 KiB before and after every allocation) were overwritten.
+ * A release build returns PHG_ERR_STATE. */
+phg_status phg_debug_checks(int64_t* dcheck_violations, int64_t* first_site,
+                            int64_t* guard_violations);
+/* 1 in the checked build, else 0 */
+int phg_is_checked_build(void);
 
 /* Accepted integration steps of the last phg_trace, phg_trace_rows (waits for its stream) or
  * phg_trace_to_host call on the context:

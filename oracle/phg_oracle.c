@@ -39,6 +39,7 @@ typedef struct {
     int32_t probe_steps;
     int32_t coast_steps;
     int32_t strict;
+    double turn_cos; /* opt-in angle stop (our extension, not the reference): -2 = off */
 } oracle_params;
 
 typedef struct {
@@ -211,6 +212,8 @@ static int step_one(const oracle_field *F, const oracle_params *P, strand_state 
     int64_t vz = floor_to_i64((tz - F->oz) / F->vs);
     int inb = vx >= 0 && vx < F->nx && vy >= 0 && vy < F->ny && vz >= 0 && vz < F->nz;
     if (!inb) die = 1;
+    /* opt-in angle stop (PHG_FLAG_TURN_STOP; the reference has none) */
+    if (dot3(s->dx, s->dy, s->dz, sx, sy, sz) < P->turn_cos) die = 1;
     int new_vox = vx != s->lvx || vy != s->lvy || vz != s->lvz;
     int full = 0;
     if (inb) {

@@ -8,6 +8,7 @@ may import this module.
 from __future__ import annotations
 
 import ctypes
+import math
 import os
 import subprocess
 
@@ -21,7 +22,7 @@ class _Params(ctypes.Structure):
     _fields_ = [("step_mm", ctypes.c_double), ("min_support", ctypes.c_double),
                 ("steer", ctypes.c_double), ("max_vertices", ctypes.c_int32),
                 ("probe_steps", ctypes.c_int32), ("coast_steps", ctypes.c_int32),
-                ("strict", ctypes.c_int32)]
+                ("strict", ctypes.c_int32), ("turn_cos", ctypes.c_double)]
 
 
 _lib = None
@@ -47,9 +48,11 @@ def _p(a):
 
 
 def _params(p):
+    deg = float(getattr(p, "max_turn_deg", 0.0) or 0.0)
+    turn = math.cos(math.radians(deg)) if 0.0 < deg < 180.0 else -2.0
     return _Params(float(p.step_mm), float(p.min_support), float(getattr(p, "steer", 0.0)),
                    int(p.max_vertices), int(p.probe_steps), int(p.coast_steps),
-                   int(bool(getattr(p, "strict", False))))
+                   int(bool(getattr(p, "strict", False))), turn)
 
 
 def trace(origin, voxel_size, occ, ori, seed_pos, seed_dir, params, at_cap=None,

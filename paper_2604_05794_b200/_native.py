@@ -14,11 +14,15 @@ import os
 from .errors import ConfigError, DataError, PipelineError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libphg_b200.so")
+# PHG_CHECKED_LIB=1 loads the checked build (device index checks + allocation canaries, the
+# stand-in for compute-sanitizer; see include/phg_b200.h phg_debug_checks)
+CHECKED = os.environ.get("PHG_CHECKED_LIB", "") == "1"
+LIB_PATH = os.path.join(HERE, "libphg_b200_checked.so" if CHECKED else "libphg_b200.so")
 
 PHG_OK, PHG_ERR_INVALID, PHG_ERR_CUDA, PHG_ERR_OOM, PHG_ERR_CAPACITY, PHG_ERR_STATE = range(6)
 PHG_FLAG_STRICT = 0x1
 PHG_FLAG_NO_ORDER = 0x2
+PHG_FLAG_TURN_STOP = 0x4
 
 # every symbol include/phg_b200.h declares (checked by tests/test_native_abi.py)
 EXPORTS = (
@@ -30,6 +34,7 @@ EXPORTS = (
     "phg_trace_to_host", "phg_stnd_encode", "phg_field_from_oovl", "phg_link", "phg_link_fetch",
     "phg_grow_begin", "phg_grow_scalp_batch", "phg_grow_field_begin", "phg_grow_field_batch",
     "phg_grow_commits", "phg_grow_apply", "phg_grow_end", "phg_trace_rows",
+    "phg_debug_checks", "phg_is_checked_build",
 )
 
 
@@ -54,6 +59,7 @@ class Params(ctypes.Structure):
         ("probe_steps", ctypes.c_int32),
         ("coast_steps", ctypes.c_int32),
         ("flags", ctypes.c_uint32),
+        ("max_turn_cos", ctypes.c_double),
     ]
 
 
@@ -116,6 +122,9 @@ def _declare(lib):
         "phg_link": (S, [VP, VP, VP, VP, VP, I64, VP, I64, ctypes.POINTER(LinkParams),
                          ctypes.POINTER(I64), VP]),
         "phg_link_fetch": (S, [VP, VP, VP, VP, VP, VP, VP, VP]),
+        "phg_debug_checks": (S, [ctypes.POINTER(I64), ctypes.POINTER(I64),
+                                 ctypes.POINTER(I64)]),
+        "phg_is_checked_build": (ctypes.c_int, []),
         "phg_field_from_oovl": (S, [ctypes.POINTER(VP), VP, VP, I64, I64, I64, I64,
                                     ctypes.POINTER(ctypes.c_double), ctypes.c_double, VP]),
     }
@@ -163,5 +172,20 @@ def params_struct(p, strict=None, order=True) -> Params:
         raise ConfigError(f"max_vertices must be >= 1 (got {mv})")
     st = bool(p.strict) if strict is None else strict
     flags = (PHG_FLAG_STRICT if st else 0) | (0 if order else PHG_FLAG_NO_ORDER)
+    turn_cos = turn_stop_cos(p)
+    if turn_cos is not None:
+        flags |= PHG_FLAG_TURN_STOP
     return Params(float(p.step_mm), float(p.min_support), float(getattr(p, "steer", 0.0)), mv,
-                  int(p.probe_steps), int(p.coast_steps), flags)
+                  int(p.probe_steps), int(p.coast_steps), flags,
+                  turn_cos if turn_cos is not None else -2.0)
+
+
+def turn_stop_cos(p):
+    """cos of the opt-in angle stop's limit, or None when it is off: ``max_turn_deg`` (an
+    extension of PhgParams, not a reference field) in (0, 180); 0 / absent = off."""
+    import math
+
+    deg = float(getattr(p, "max_turn_deg", 0.0) or 0.0)
+    if deg <= 0.0 or deg >= 180.0:
+        return None
+    return math.cos(math.radians(deg))

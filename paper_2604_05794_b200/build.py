@@ -17,6 +17,7 @@ SRCS = [os.path.join(HERE, "csrc", f)
         for f in ("phg_trace.cu", "phg_grow.cu", "phg_link.cu", "phg_io.cu", "phg_copy.cu")]
 HDRS = [os.path.join(HERE, "csrc", "phg_core.cuh")]
 OUT = os.path.join(HERE, "libphg_b200.so")
+OUT_CHECKED = os.path.join(HERE, "libphg_b200_checked.so")
 
 NVCC_FLAGS = [
     "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
@@ -31,20 +32,24 @@ def nvcc():
     return cand
 
 
-def build(force=False, verbose=False):
+def build(force=False, verbose=False, checked=False):
+    """checked=True: libphg_b200_checked.so with -DPHG_CHECKED (device index checks and
+    allocation canaries; loaded with PHG_CHECKED_LIB=1)."""
+    out = OUT_CHECKED if checked else OUT
     deps = SRCS + HDRS + [os.path.join(ROOT, "include", "phg_b200.h")]
-    if (not force and os.path.exists(OUT)
-            and os.path.getmtime(OUT) >= max(os.path.getmtime(d) for d in deps)):
-        return OUT
-    cmd = [nvcc(), *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-o", OUT, *SRCS]
+    if (not force and os.path.exists(out)
+            and os.path.getmtime(out) >= max(os.path.getmtime(d) for d in deps)):
+        return out
+    flags = NVCC_FLAGS + (["-DPHG_CHECKED"] if checked else [])
+    cmd = [nvcc(), *flags, "-I", os.path.join(ROOT, "include"), "-o", out, *SRCS]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError(f"nvcc failed ({r.returncode})")
     if verbose:
         sys.stderr.write(r.stderr)
-    return OUT
+    return out
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    print(build(force="--force" in sys.argv, verbose=True, checked="--checked" in sys.argv))

@@ -373,10 +373,7 @@ __global__ void u32_to_u16(const uint32_t* __restrict__ a, uint16_t* __restrict_
         b[i] = (uint16_t)(a[i] & 0xffffu);
 }
 
-void swap_buf(DevBuf& a, DevBuf& b) {
-    std::swap(a.p, b.p);
-    std::swap(a.cap, b.cap);
-}
+void swap_buf(DevBuf& a, DevBuf& b) { a.swap(b); }
 
 // ---- speculative deferred-commit batches ------------------------------------------------------
 // Every batch of a phase is traced in ONE launch against the cap plane P0 at the start of the

@@ -158,6 +158,11 @@ phg_status phg_field_from_oovl(phg_field** out, const uint8_t* bits, const float
         delete f;
         return fail(PHG_ERR_CUDA, "oovl_scatter_kernel: %s", cudaGetErrorString(e));
     }
+    s = field_build_bricks(f, st);
+    if (s != PHG_OK) {
+        delete f;
+        return s;
+    }
     *out = f;
     return PHG_OK;
 }

@@ -52,6 +52,10 @@ class PhgParams:
     smooth_iters: int = 2
     strict: bool = False
     tangent_window: int = 3
+    # extension, not a reference field: opt-in angle stop (degrees; 0 = off, the reference's
+    # behaviour).  A step turning by more than this from the previous step direction ends the
+    # strand (PHG_FLAG_TURN_STOP in include/phg_b200.h).
+    max_turn_deg: float = 0.0
 
     def __post_init__(self):
         if self.link_dist_mm <= 0:
@@ -60,6 +64,8 @@ class PhgParams:
             raise ConfigError("link_angle_deg must be in (0, 90)")
         if self.step_mm <= 0 or self.batch_size < 1 or self.occupancy_cap < 1:
             raise ConfigError("invalid tracing parameters")
+        if not (0.0 <= self.max_turn_deg <= 180.0):
+            raise ConfigError("max_turn_deg must be in [0, 180] (0 = off)")
 
 
 class Tracer:

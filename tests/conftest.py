@@ -49,3 +49,24 @@ def oracle_c():
 
     phg_oracle_c.build()
     return phg_oracle_c
+
+
+@pytest.fixture(autouse=True)
+def _checked_build_guard(request):
+    """With PHG_CHECKED_LIB=1 (the checked build, our compute-sanitizer stand-in) every GPU
+    test must leave zero device index-check violations and intact allocation canaries."""
+    yield
+    if os.environ.get("PHG_CHECKED_LIB") != "1" or request.node.get_closest_marker("gpu") is None:
+        return
+    import ctypes
+
+    from paper_2604_05794_b200 import _native
+
+    lib = _native.load()
+    assert lib.phg_is_checked_build() == 1
+    v, site, g = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+    _native.check(lib.phg_debug_checks(ctypes.byref(v), ctypes.byref(site), ctypes.byref(g)),
+                  "phg_debug_checks")
+    assert v.value == 0 and g.value == 0, (
+        f"checked build: {v.value} device index-check violations (first site {site.value}), "
+        f"{g.value} buffers with overwritten canaries {lib.phg_last_error().decode()}")

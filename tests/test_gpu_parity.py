@@ -551,3 +551,76 @@ def test_rows_api_equals_csr_and_oracle(gpu, oracle_c, count, cap):
     off_o, v_o = oracle_c.to_csr(slab, keep)
     assert np.array_equal(off_o, off) and np.array_equal(v_o, v)
     assert tr.last_steps() >= rs.steps  # accepted steps include trimmed trailing coasts
+
+
+@pytest.mark.parametrize("kind,deg", [("curly", 4.0), ("sparse", 10.0), ("wavy", 2.0)])
+def test_opt_in_turn_stop(gpu, oracle_c, kind, deg):
+    """The opt-in angle stop (PhgParams.max_turn_deg, PHG_FLAG_TURN_STOP; not in the
+    reference): off (0) leaves every output identical to the reference semantics; on, the
+    CUDA path equals the C oracle's restatement of the same rule bit for bit and stops some
+    strands earlier."""
+    vol, s, d, p = _config_case(kind, 48, 6_000, 41, interior=1_000 if kind == "sparse" else 0)
+    base = gpu.phg.trace_batch_csr(vol, s, d, p)
+    off0 = gpu.phg.trace_batch_csr(vol, s, d, SimpleNamespace(**vars(p), max_turn_deg=0.0))
+    assert all(np.array_equal(a, b) for a, b in zip(base, off0))
+    pt = SimpleNamespace(**vars(p), max_turn_deg=deg)
+    for cap in (None, np.random.default_rng(2).random(vol.occ.shape) < 0.02):
+        off, v, ent = gpu.phg.trace_batch_csr(vol, s, d, pt, at_cap=cap)
+        slab, keep, ent_o = oracle_c.trace(vol.origin, vol.voxel_size, vol.occ, vol.ori, s, d, pt,
+                                           at_cap=cap)
+        off_o, v_o = oracle_c.to_csr(slab, keep)
+        assert np.array_equal(off, off_o) and np.array_equal(v, v_o)
+        assert np.array_equal(ent, ent_o)
+    assert len(v) < len(base[1]), "the angle stop never fired"
+
+
+@pytest.mark.parametrize("kind,n,dims", [("sparse", 64, None), ("curly", 48, None),
+                                         ("sparse", 40, (37, 41, 43))])
+def test_bricked_sampler_bit_exact(gpu, oracle_c, monkeypatch, kind, n, dims):
+    """The bricked copy of a sparse field (4^3 bricks with a +1 apron, empty bricks aliased to
+    one zero brick; kSmpBrick*) traces bit-identically to the oracle, with and without a cap
+    plane and the angle stop, on dims that are not multiples of the brick edge."""
+    vol, s, d, p = _config_case(kind, n, 5_000, 51, interior=1_500 if kind == "sparse" else 0)
+    if dims is not None:  # crop to odd dims (seeds outside the crop die at once, as they should)
+        vol.occ = np.ascontiguousarray(vol.occ[: dims[0], : dims[1], : dims[2]])
+        vol.ori = np.ascontiguousarray(vol.ori[: dims[0], : dims[1], : dims[2]])
+        vol.dims = vol.occ.shape
+    monkeypatch.setenv("PHG_BRICKS", "1")
+    gpu.volume.invalidate()
+    tr = gpu.phg._tracer()
+    cap = np.random.default_rng(9).random(vol.occ.shape) < 0.02
+    for plane in (None, cap):
+        for pp in (p, SimpleNamespace(**vars(p), max_turn_deg=8.0)):
+            off, v, ent = gpu.phg.trace_batch_csr(vol, s, d, pp, at_cap=plane)
+            assert tr.last_sampler().startswith("brick"), tr.last_sampler()
+            slab, keep, ent_o = oracle_c.trace(vol.origin, vol.voxel_size, vol.occ, vol.ori, s, d,
+                                               pp, at_cap=plane)
+            off_o, v_o = oracle_c.to_csr(slab, keep)
+            assert np.array_equal(off, off_o) and np.array_equal(v, v_o)
+            assert np.array_equal(ent, ent_o)
+    monkeypatch.setenv("PHG_BRICKS", "0")
+    gpu.volume.invalidate()
+    gpu.phg.trace_batch_csr(vol, s[:10], d[:10], p)
+    assert not tr.last_sampler().startswith("brick")
+    gpu.volume.invalidate()
+
+
+def test_bricked_driver_bit_exact(gpu, monkeypatch):
+    """The device batch driver (speculative windows, recording traces) on a bricked field
+    reproduces the reference's init_guide_strands fixtures."""
+    from paper_2604_05794_b200 import grow
+    from paper_2604_05794_b200.phg import PhgParams
+    from paper_2604_05794_b200.volume import OOVolume
+
+    monkeypatch.setenv("PHG_BRICKS", "1")
+    gpu.volume.invalidate()
+    for name in ("driver_sparse40", "driver_curly32_cap1"):
+        c = load_case(os.path.join(GOLDEN, f"{name}.npz"))
+        vol = OOVolume.empty(c.origin, float(c.voxel_size), c.occ.shape)
+        vol.occ, vol.ori = c.occ, c.ori
+        prm = PhgParams(**{k: v for k, v in vars(c.params).items()
+                           if k in PhgParams.__dataclass_fields__})
+        off, verts, rooted, rep = grow.init_guide_strands_csr(c.seeds, c.dirs, vol, prm)
+        assert np.array_equal(off, c.offsets) and np.array_equal(verts, c.verts)
+        assert np.array_equal(rooted, c.rooted) and np.array_equal(vol.counts, c.counts_out)
+    gpu.volume.invalidate()

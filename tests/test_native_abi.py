@@ -38,7 +38,7 @@ def test_library_exports_every_header_symbol(lib):
 
 
 def test_abi_version(lib):
-    assert lib.phg_abi_version() == 1
+    assert lib.phg_abi_version() == 2
 
 
 def test_null_arguments_fail_cleanly_without_gpu(lib):
