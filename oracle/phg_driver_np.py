@@ -25,8 +25,15 @@ def _commit(counts, origin, vs, dims, v):
     counts[u[:, 0], u[:, 1], u[:, 2]] += 1
 
 
-def init_guide(origin, vs, occ, ori, counts, seeds, normals, params, near_occ=None):
-    """Returns ([(vertices, rooted), ...], report); updates ``counts`` (uint16) in place."""
+def init_guide(origin, vs, occ, ori, counts, seeds, normals, params, near_occ=None,
+               trace_batch=None):
+    """Returns ([(vertices, rooted), ...], report); updates ``counts`` (uint16) in place.
+
+    ``trace_batch`` (optional): a function with the reference's trace_batch signature
+    (vol, seed_pos, seed_dir, params, at_cap=None, live_counts=None, near_occ=None) ->
+    [(vertices, entered), ...] that replaces the C oracle trace -- the GPU tests pass the
+    drop-in ``paper_2604_05794_b200.phg.trace_batch`` to run the reference's batch loop
+    (phg.py:229-251, 277-302) over it, exactly as strandkit.phg does after install()."""
     origin = np.asarray(origin, np.float64)
     dims = occ.shape
     strict = bool(params.strict)
@@ -37,8 +44,17 @@ def init_guide(origin, vs, occ, ori, counts, seeds, normals, params, near_occ=No
         return [], report
     out = []
 
+    if trace_batch is not None:  # one volume object for the whole loop, as the reference has
+        from types import SimpleNamespace
+
+        vol = SimpleNamespace(origin=origin, voxel_size=vs, dims=occ.shape, occ=occ, ori=ori,
+                              counts=counts)
+
     def run(pos, dirs):
         cap = None if strict else (counts >= params.occupancy_cap)
+        if trace_batch is not None:
+            return trace_batch(vol, pos, dirs, params, at_cap=None if strict else cap,
+                               live_counts=counts if strict else None, near_occ=near)
         slab, keep, ent = oc.trace(origin, vs, occ, ori, pos, dirs, params, at_cap=cap,
                                    live_counts=counts if strict else None, near_occ=near)
         return [(slab[i, : keep[i]].copy(), bool(ent[i])) for i in range(len(keep))]

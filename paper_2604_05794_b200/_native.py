@@ -18,6 +18,11 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 # stand-in for compute-sanitizer; see include/phg_b200.h phg_debug_checks)
 CHECKED = os.environ.get("PHG_CHECKED_LIB", "") == "1"
 LIB_PATH = os.path.join(HERE, "libphg_b200_checked.so" if CHECKED else "libphg_b200.so")
+# PHG_LIB_PATH=<file>: load another build of the library (A/B timing of kernel changes on one
+# box); symbols that build lacks are left undeclared
+_OVERRIDE = os.environ.get("PHG_LIB_PATH", "")
+if _OVERRIDE:
+    LIB_PATH = os.path.abspath(_OVERRIDE)
 
 PHG_OK, PHG_ERR_INVALID, PHG_ERR_CUDA, PHG_ERR_OOM, PHG_ERR_CAPACITY, PHG_ERR_STATE = range(6)
 PHG_FLAG_STRICT = 0x1
@@ -129,6 +134,8 @@ def _declare(lib):
                                     ctypes.POINTER(ctypes.c_double), ctypes.c_double, VP]),
     }
     for name, (res, args) in sig.items():
+        if _OVERRIDE and not hasattr(lib, name):
+            continue
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args

@@ -247,3 +247,40 @@ def test_speculative_driver_equals_sequential(monkeypatch, cap, kind, window):
     assert np.array_equal(off_s, off_q) and np.array_equal(r_s, r_q)
     assert np.array_equal(v_s, v_q)
     assert np.array_equal(counts_s, counts_q)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("path", DRIVER_CASES, ids=lambda p: os.path.basename(p)[7:-4])
+def test_reference_batch_loop_over_dropin_trace_batch(path, oracle_c):
+    """The reference's own init_guide_strands batch loop (restated in oracle/phg_driver_np.py:
+    per-batch frozen at_cap plane, commits, field-seed pass with +d/-d joins, strict
+    live_counts) calling the drop-in ``phg.trace_batch`` on the GPU -- what strandkit.phg runs
+    after install() -- reproduces the reference's fixtures: per-batch set_cap uploads, the
+    field cache reused across batches of one volume, strict mode's in-place live_counts."""
+    from oracle import phg_driver_np as dn
+    from paper_2604_05794_b200 import phg, volume
+
+    c = load_case(path)
+    counts = np.zeros(c.occ.shape, np.uint16)
+    near = near_map(c.occ) if c.params.steer > 0 else None
+    uploads = []
+    real = volume.DeviceField
+
+    class Counting(real):
+        def __init__(self, *a, **k):
+            uploads.append(1)
+            super().__init__(*a, **k)
+
+    volume.DeviceField = Counting
+    try:
+        out, rep = dn.init_guide(c.origin, float(c.voxel_size), c.occ, c.ori, counts, c.seeds,
+                                 c.dirs, c.params, near_occ=near, trace_batch=phg.trace_batch)
+    finally:
+        volume.DeviceField = real
+    off, verts, rooted = _csr(out)
+    assert np.array_equal(off, c.offsets)
+    assert np.array_equal(verts, c.verts)
+    assert np.array_equal(rooted, c.rooted)
+    assert np.array_equal(counts, c.counts_out)
+    assert rep == json.loads(str(c.report))
+    assert len(uploads) == 1  # one field upload for the whole loop (field cache)
