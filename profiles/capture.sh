@@ -25,4 +25,6 @@ for cfg in "$@"; do
     "python bench.py --config $cfg --steps 1 --warmup 1 --no-e2e --no-cpu --no-driver" \
     "$steps" > "$out/summary_$cfg.txt" 2>&1
   echo "$cfg: steps=$steps $(head -c 300 "$out/summary_$cfg.txt" | tr '\n' ' ')"
+  # reports are tens of MB: keep the summary only (gpurun copies back <= 64 MiB)
+  [ "${KEEP_REP:-0}" = 1 ] || rm -f "$out/trace_$cfg.ncu-rep"
 done

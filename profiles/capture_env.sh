@@ -13,3 +13,4 @@ python profiles/summarize_ncu.py "$out/trace_${cfg}_$label.ncu-rep" "$out/ncu_${
   "trace_kernel $label, $cfg" "$* python bench.py --config $cfg --steps 1 --warmup 1 --no-e2e --no-cpu --no-driver" \
   "$steps" > "$out/summary_${cfg}_$label.txt" 2>&1
 head -c 400 "$out/summary_${cfg}_$label.txt"; echo
+[ "${KEEP_REP:-0}" = 1 ] || rm -f "$out/trace_${cfg}_$label.ncu-rep"
