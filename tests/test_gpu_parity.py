@@ -624,3 +624,31 @@ def test_bricked_driver_bit_exact(gpu, monkeypatch):
         assert np.array_equal(off, c.offsets) and np.array_equal(verts, c.verts)
         assert np.array_equal(rooted, c.rooted) and np.array_equal(vol.counts, c.counts_out)
     gpu.volume.invalidate()
+
+
+@pytest.mark.parametrize("kind", ["sparse", "curly"])
+def test_strict_cooperative_equals_per_step_launches(gpu, oracle_c, monkeypatch, kind):
+    """Strict mode in one cooperative launch (grid barriers between each step and its
+    commits, early exit) equals the per-step launch pairs and the C oracle bit for bit,
+    including the in-place live_counts (phg.py:136-155)."""
+    vol, s, d, p = _config_case(kind, 48, 3_000, 61, interior=800 if kind == "sparse" else 0)
+    p = SimpleNamespace(**vars(p))
+    p.strict = True
+    outs = []
+    for coop in ("1", "0"):
+        monkeypatch.setenv("PHG_STRICT_COOP", coop)
+        counts = np.zeros(vol.occ.shape, np.uint16)
+        counts[::3, ::5, ::7] = 1
+        res = gpu.phg.trace_batch_csr(vol, s, d, p, live_counts=counts)
+        outs.append((res, counts))
+        assert gpu.phg._tracer().last_variant() == ("strict/cooperative" if coop == "1"
+                                                    else "strict")
+    (a, ca), (b, cb) = outs
+    assert all(np.array_equal(x, y) for x, y in zip(a, b)) and np.array_equal(ca, cb)
+    counts = np.zeros(vol.occ.shape, np.uint16)
+    counts[::3, ::5, ::7] = 1
+    slab, keep, ent = oracle_c.trace(vol.origin, vol.voxel_size, vol.occ, vol.ori, s, d, p,
+                                     live_counts=counts)
+    off_o, v_o = oracle_c.to_csr(slab, keep)
+    assert np.array_equal(a[0], off_o) and np.array_equal(a[1], v_o)
+    assert np.array_equal(counts, ca)
