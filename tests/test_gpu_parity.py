@@ -652,3 +652,60 @@ def test_strict_cooperative_equals_per_step_launches(gpu, oracle_c, monkeypatch,
     off_o, v_o = oracle_c.to_csr(slab, keep)
     assert np.array_equal(a[0], off_o) and np.array_equal(a[1], v_o)
     assert np.array_equal(counts, ca)
+
+
+def _fuzz_field(rng, dims, fill, noise_ori):
+    occ = rng.random(dims) < fill
+    ori = rng.normal(size=dims + (3,)).astype(np.float32)
+    ori /= np.linalg.norm(ori, axis=-1, keepdims=True).astype(np.float32)
+    if noise_ori:  # unoccupied voxels with garbage (finite) orientations: the fast sampler
+        ori[~occ] *= 7.5  # must still ignore them (packed as 0 where unoccupied)
+    else:
+        ori[~occ] = 0
+    return occ, ori
+
+
+def _fuzz_points(rng, dims, vs, m):
+    hi = np.array(dims) * vs
+    pts = rng.uniform(-0.3 * hi, 1.3 * hi, size=(m, 3))     # inside and around the field
+    k = m // 4
+    pts[:k] = np.round(pts[:k] / (vs / 2)) * (vs / 2)          # exactly on voxel faces/centres
+    pts[k:k + 8] = [[0, 0, 0], hi, [hi[0], 0, 0], [0, hi[1], 0], [0, 0, hi[2]],
+                    [-vs, -vs, -vs], [1e300, 0, 0], [-1e300, 5, 5]]
+    return pts
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_fuzz_sampler_and_trace_bit_exact(gpu, oracle_c, seed):
+    """Randomised fields (odd dims, non-power-of-two voxel sizes, occupied fractions from
+    sparse to dense, garbage orientations in empty voxels) and points / seeds inside, outside,
+    exactly on voxel faces and far away, with random and zero directions: the CUDA sampler
+    equals the numpy restatement of sample_orientation_batch (volume.py:190-224) and the CUDA
+    trace equals the C oracle, bit for bit, with and without a cap plane."""
+    from oracle import phg_oracle_np as onp
+
+    rng = np.random.default_rng(seed)
+    dims = tuple(int(x) for x in rng.integers(5, 40, size=3))
+    vs = float(rng.choice([0.5, 1.0, 1.3, 2.0, 2.7]))
+    occ, ori = _fuzz_field(rng, dims, float(rng.uniform(0.1, 0.9)), seed % 2 == 1)
+    origin = rng.uniform(-5, 5, size=3)
+    vol = SimpleNamespace(origin=origin, voxel_size=vs, dims=dims, occ=occ, ori=ori)
+    pts = _fuzz_points(rng, dims, vs, 20_000) + origin
+    prev = rng.normal(size=pts.shape)
+    prev[::7] = 0.0
+    d, h, s = gpu.volume.sample_orientation_batch(vol, pts, prev)
+    f = onp.Field(origin, vs, dims, occ, ori)
+    d_o, h_o, s_o = onp.sample(f, pts, prev)
+    assert np.array_equal(h, h_o) and np.array_equal(s, s_o) and np.array_equal(d, d_o)
+    seeds = _fuzz_points(rng, dims, vs, 6_000)[8:] + origin  # finite seeds
+    dirs = rng.normal(size=seeds.shape)
+    dirs[::11] = 0.0
+    p = SimpleNamespace(step_mm=float(rng.choice([0.4, 1.0, 1.7])), max_vertices=int(
+        rng.choice([2, 57, 400])), min_support=float(rng.choice([0.0, 0.05, 0.3])),
+        probe_steps=int(rng.integers(0, 30)), coast_steps=int(rng.integers(0, 30)), steer=0.0,
+        strict=False)
+    for cap in (None, rng.random(dims) < 0.05):
+        off, v, ent = gpu.phg.trace_batch_csr(vol, seeds, dirs, p, at_cap=cap)
+        slab, keep, ent_o = oracle_c.trace(origin, vs, occ, ori, seeds, dirs, p, at_cap=cap)
+        off_o, v_o = oracle_c.to_csr(slab, keep)
+        assert np.array_equal(off, off_o) and np.array_equal(v, v_o) and np.array_equal(ent, ent_o)
