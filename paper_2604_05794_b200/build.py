@@ -10,6 +10,8 @@ import os
 import shutil
 import subprocess
 import sys
+import tempfile
+from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
@@ -21,7 +23,7 @@ OUT_CHECKED = os.path.join(HERE, "libphg_b200_checked.so")
 
 NVCC_FLAGS = [
     "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
-    "-fmad=false", "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v",
+    "-fmad=false", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
 ]
 
 
@@ -32,23 +34,51 @@ def nvcc():
     return cand
 
 
+def _compile(args):
+    src, obj, flags = args
+    cmd = [nvcc(), *flags, "-I", os.path.join(ROOT, "include"), "-c", "-o", obj, src]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    return src, r
+
+
 def build(force=False, verbose=False, checked=False):
     """checked=True: libphg_b200_checked.so with -DPHG_CHECKED (device index checks and
-    allocation canaries; loaded with PHG_CHECKED_LIB=1)."""
+    allocation canaries; loaded with PHG_CHECKED_LIB=1).  The translation units compile in
+    parallel (one nvcc per file), then link into the shared library."""
     out = OUT_CHECKED if checked else OUT
     deps = SRCS + HDRS + [os.path.join(ROOT, "include", "phg_b200.h")]
     if (not force and os.path.exists(out)
             and os.path.getmtime(out) >= max(os.path.getmtime(d) for d in deps)):
         return out
     flags = NVCC_FLAGS + (["-DPHG_CHECKED"] if checked else [])
-    cmd = [nvcc(), *flags, "-I", os.path.join(ROOT, "include"), "-o", out, *SRCS]
-    r = subprocess.run(cmd, capture_output=True, text=True)
-    if r.returncode != 0:
-        sys.stderr.write(r.stdout + r.stderr)
-        raise RuntimeError(f"nvcc failed ({r.returncode})")
-    if verbose:
-        sys.stderr.write(r.stderr)
+    objdir = tempfile.mkdtemp(prefix="phg_build_")
+    try:
+        jobs = [(src, os.path.join(objdir, os.path.basename(src) + ".o"), flags) for src in SRCS]
+        with ThreadPoolExecutor(max_workers=len(jobs)) as ex:
+            results = list(ex.map(_compile, jobs))
+        for src, r in results:
+            if r.returncode != 0:
+                sys.stderr.write(r.stdout + r.stderr)
+                raise RuntimeError(f"nvcc failed on {os.path.basename(src)} ({r.returncode})")
+            if verbose:
+                sys.stderr.write(r.stderr)
+        tmp_out = out + ".tmp"
+        link = [nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-Xcompiler",
+                "-fPIC", "-o", tmp_out, *[j[1] for j in jobs]]
+        r = subprocess.run(link, capture_output=True, text=True)
+        if r.returncode != 0:
+            sys.stderr.write(r.stdout + r.stderr)
+            raise RuntimeError(f"nvcc link failed ({r.returncode})")
+        os.replace(tmp_out, out)  # atomic: a loaded library is never half-written
+    finally:
+        shutil.rmtree(objdir, ignore_errors=True)
     return out
+
+
+def build_all(force=False):
+    """The release and the checked library, concurrently."""
+    with ThreadPoolExecutor(max_workers=2) as ex:
+        return list(ex.map(lambda c: build(force=force, checked=c), (False, True)))
 
 
 if __name__ == "__main__":
