@@ -282,7 +282,7 @@ def cpu_legs(cfg, ori, occ, seeds, dirs, cores, model, one_core=True, c_port=Tru
 def host_field(cfg):
     from paper_2604_05794_b200 import synth
 
-    ori, occ = synth.make_field(cfg.kind, cfg.n, "cpu")
+    ori, occ = cfg.field("cpu")
     return ori.numpy(), occ.numpy()
 
 
@@ -297,7 +297,7 @@ def run_reference(args):
     cfg = synth.CONFIGS[resolve_config(args, ws)]
     cores, model = cpu_host_info()
     params = PhgParams(field_seeds=0)
-    ori_t, occ_t = synth.make_field(cfg.kind, cfg.n, "cpu")
+    ori_t, occ_t = cfg.field("cpu")
     seeds, dirs = cpu_sample_seeds(cfg, args, ori_t, occ_t)
     ori, occ = ori_t.numpy(), occ_t.numpy()
     del ori_t, occ_t
@@ -474,7 +474,7 @@ def run_ours(args):
     params = phg.PhgParams(field_seeds=0, batch_size=per_rank * ws)
 
     # field generated directly in HBM, packed once (replicated per rank)
-    ori, occ = synth.make_field(cfg.kind, cfg.n, dev)
+    ori, occ = cfg.field(dev)
     field = DeviceField(np.zeros(3), synth.VOXEL_MM, occ, ori,
                         torch.cuda.current_stream(dev).cuda_stream)
     ori_host = occ_host = None

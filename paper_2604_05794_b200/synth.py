@@ -34,6 +34,11 @@ class Config:
     seeds: int          # seeds per GPU (scalp disk; sparse adds interior seeds)
     key: int            # Philox key for the seeds
     note: str
+    omega_turns: float = 24.0  # curly / sparse fields: vortex rate W = omega_turns * pi / L
+
+    def field(self, device="cpu"):
+        """(ori, occ) of this config (make_field with the config's parameters)."""
+        return make_field(self.kind, self.n, device, omega_turns=self.omega_turns)
 
 
 CONFIGS = {
@@ -42,6 +47,11 @@ CONFIGS = {
     "C3": Config("C3", 512, "curly", 1_000_000, 13, "512^3 curly vortex cylinder, 1M seeds"),
     "C4": Config("C4", 512, "curly", 4_000_000, 14, "512^3 curly, 4M seeds split over ranks"),
     "C5": Config("C5", 1024, "sparse", 8_000_000, 15, "1024^3 10%-fill sparse, scalp+interior"),
+    # not a BASELINE config: C3 with a 6x slower vortex (W = 4 pi / L), so the helices climb
+    # ~6x higher instead of winding near the seed plane (strand tops p50: C3 ~9 voxels, C3s
+    # ~56): a stress case with a larger field footprint, measured beside C3
+    "C3s": Config("C3s", 512, "curly", 1_000_000, 13, "512^3 steep curly (W = 4 pi/L), 1M seeds",
+                  omega_turns=4.0),
 }
 
 

@@ -36,7 +36,7 @@ def main():
     cfg = synth.CONFIGS[name]
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)
-    ori, occ = synth.make_field(cfg.kind, cfg.n, dev)
+    ori, occ = cfg.field(dev)
     stream = torch.cuda.current_stream(dev)
     field = DeviceField(np.zeros(3), synth.VOXEL_MM, occ, ori, stream.cuda_stream)
     seeds, dirs = synth.config_seeds(cfg, 1_000_000, ori, occ)

@@ -18,7 +18,7 @@ from paper_2604_05794_b200.volume import OOVolume  # noqa: E402
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 200_000
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 2
 cfg = synth.CONFIGS["C3"]
-ori, occ = synth.make_field(cfg.kind, cfg.n, "cuda")
+ori, occ = cfg.field("cuda")
 vol = OOVolume.empty((0, 0, 0), synth.VOXEL_MM, occ.shape)
 vol.ori, vol.occ = ori.cpu().numpy(), occ.cpu().numpy()
 del ori, occ
