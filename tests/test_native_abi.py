@@ -97,3 +97,28 @@ def test_product_package_never_imports_oracle():
             if f.endswith(".py"):
                 src = open(os.path.join(dirpath, f)).read()
                 assert "oracle" not in re.sub(r"#.*|\"\"\"[\s\S]*?\"\"\"", "", src), f
+
+
+def test_default_trace_kernels_do_not_spill():
+    """The default trace kernels (every sampler mode, cap / no cap, the driver's recording
+    traces) fit their register budget without local-memory spills: a spill is a silent
+    performance regression (round 1 measured +11% for 70-94 B of spills)."""
+    import subprocess
+
+    from paper_2604_05794_b200 import build
+
+    build.build()
+    out = subprocess.run(["cuobjdump", "-res-usage", build.OUT], capture_output=True, text=True)
+    if out.returncode != 0:
+        pytest.skip("cuobjdump unavailable")
+    lines = out.stdout.splitlines()
+    default = "trace_kernelINS_3CfgILi1ELi1ELi4ELi8ELi128ELb1ELi4ELb1EEE"
+    seen = 0
+    for i, ln in enumerate(lines):
+        if "Function" in ln and default in ln:
+            res = lines[i + 1]
+            seen += 1
+            reg = int(re.search(r"REG:(\d+)", res).group(1))
+            assert "LOCAL:0" in res and "STACK:0" in res, (ln, res)
+            assert reg <= 128, (ln, res)  # 4 CTAs of 128 threads per SM
+    assert seen >= 12, seen
