@@ -1126,6 +1126,7 @@ phg_status phg_grow_begin(phg_ctx* c, phg_field* f, const phg_params_v1* p,
 
 phg_status phg_grow_scalp_batch(phg_ctx* c, const double* seeds, const double* normals,
                                 int64_t nb, int32_t export_commits, int64_t out[2], void* stream) {
+    PHG_RANGE("phg/grow_scalp_batch");
     if (!c || !out || nb < 0 || (nb > 0 && (!seeds || !normals)))
         return fail(PHG_ERR_INVALID, "phg_grow_scalp_batch: bad argument");
     if (!session(c)) return fail(PHG_ERR_STATE, "phg_grow_scalp_batch: no phg_grow_begin");
@@ -1153,6 +1154,7 @@ phg_status phg_grow_field_begin(phg_ctx* c, int64_t* n_field_seeds, void* stream
 
 phg_status phg_grow_field_batch(phg_ctx* c, int64_t first, int64_t nb, int32_t export_commits,
                                 int64_t out[2], void* stream) {
+    PHG_RANGE("phg/grow_field_batch");
     if (!c || !out || first < 0 || nb < 0)
         return fail(PHG_ERR_INVALID, "phg_grow_field_batch: bad argument");
     if (!session(c)) return fail(PHG_ERR_STATE, "phg_grow_field_batch: no phg_grow_begin");
@@ -1179,6 +1181,7 @@ phg_status phg_grow_commits(phg_ctx* c, uint32_t* ids, void* stream) {
 }
 
 phg_status phg_grow_apply(phg_ctx* c, const uint32_t* ids, int64_t n, void* stream) {
+    PHG_RANGE("phg/grow_apply");
     if (!c || !session(c)) return fail(PHG_ERR_STATE, "phg_grow_apply: no session");
     if (n < 0 || (n > 0 && !ids)) return fail(PHG_ERR_INVALID, "phg_grow_apply: bad ids");
     GrowSession& S = *session(c);
@@ -1242,6 +1245,7 @@ phg_status phg_grow_init(phg_ctx* c, phg_field* f, const phg_params_v1* p,
                          const phg_grow_params_v1* g, const double* seeds, const double* normals,
                          int64_t n, uint16_t* counts, int64_t* n_segments, int64_t* n_verts,
                          int64_t report[4], void* stream) {
+    PHG_RANGE("phg/grow_init");
     if (!c || !f || !p || !g || !counts || !n_segments || !n_verts || !report)
         return fail(PHG_ERR_INVALID, "phg_grow_init: null argument");
     if (n < 0) return fail(PHG_ERR_INVALID, "phg_grow_init: negative seed count");

@@ -69,6 +69,7 @@ extern "C" {
 
 phg_status phg_stnd_encode(const int64_t* offsets, const double* verts, int64_t n_strands,
                            uint8_t* out, void* stream) {
+    PHG_RANGE("phg/stnd_encode");
     if (!offsets || !out || n_strands < 0) return fail(PHG_ERR_INVALID, "phg_stnd_encode: bad args");
     cudaStream_t st = as_stream(stream);
     DevBuf s_off, s_v, s_out;
@@ -98,6 +99,7 @@ phg_status phg_stnd_encode(const int64_t* offsets, const double* verts, int64_t 
 phg_status phg_field_from_oovl(phg_field** out, const uint8_t* bits, const float* ori_occupied,
                                int64_t n_occ, int64_t nx, int64_t ny, int64_t nz,
                                const double origin[3], double voxel_size, void* stream) {
+    PHG_RANGE("phg/field_from_oovl");
     if (!out || !bits || !origin || n_occ < 0)
         return fail(PHG_ERR_INVALID, "phg_field_from_oovl: null argument");
     *out = nullptr;

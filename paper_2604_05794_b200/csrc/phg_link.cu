@@ -406,6 +406,7 @@ phg_status phg_link(phg_ctx* c, const int64_t* offsets, const double* verts,
                     const uint8_t* rooted, const uint8_t* source, int64_t n,
                     const double* scalp, int64_t n_scalp, const phg_link_params_v1* lp,
                     int64_t counts_out[4], void* stream) {
+    PHG_RANGE("phg/link");
     if (!c || !lp || !counts_out || n < 0 || n_scalp < 0)
         return fail(PHG_ERR_INVALID, "phg_link: bad argument");
     if (!(lp->link_dist_mm > 0)) return fail(PHG_ERR_INVALID, "phg_link: link_dist_mm must be > 0");
