@@ -81,6 +81,20 @@ phg_status phg_field_destroy(phg_field* f);
 /* dims / device of a field (for callers' validation) */
 phg_status phg_field_info(const phg_field* f, int64_t dims[3], int* device);
 
+/* ---- field replication across GPUs (multi-GPU setup) -------------------------
+ * The packed field is one device buffer plus two scalars, so ranks can replicate it with one
+ * broadcast over NVLink instead of each rank uploading and packing the host arrays.
+ * phg_field_packed: the padded packed voxel buffer (device pointer, bytes) and its flags.
+ * phg_field_create_packed: a field of the given geometry whose packed buffer the caller then
+ *   fills (e.g. the NCCL broadcast of another rank's phg_field_packed buffer), followed by
+ *   phg_field_packed_done (derived structures, e.g. the optional bricked copy). */
+phg_status phg_field_packed(const phg_field* f, void** vox, int64_t* bytes, int32_t* zeroed,
+                            float* maxabs);
+phg_status phg_field_create_packed(phg_field** out, int64_t nx, int64_t ny, int64_t nz,
+                                   const double origin[3], double voxel_size, int32_t zeroed,
+                                   float maxabs, void* stream);
+phg_status phg_field_packed_done(phg_field* f, void* stream);
+
 /* ---- context ---------------------------------------------------------------- */
 phg_status phg_ctx_create(phg_ctx** out);
 phg_status phg_ctx_destroy(phg_ctx* c);

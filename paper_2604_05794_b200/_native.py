@@ -39,7 +39,8 @@ EXPORTS = (
     "phg_trace_to_host", "phg_stnd_encode", "phg_field_from_oovl", "phg_link", "phg_link_fetch",
     "phg_grow_begin", "phg_grow_scalp_batch", "phg_grow_field_begin", "phg_grow_field_batch",
     "phg_grow_commits", "phg_grow_apply", "phg_grow_end", "phg_trace_rows",
-    "phg_debug_checks", "phg_is_checked_build",
+    "phg_debug_checks", "phg_is_checked_build", "phg_field_packed", "phg_field_create_packed",
+    "phg_field_packed_done",
 )
 
 
@@ -130,6 +131,12 @@ def _declare(lib):
         "phg_debug_checks": (S, [ctypes.POINTER(I64), ctypes.POINTER(I64),
                                  ctypes.POINTER(I64)]),
         "phg_is_checked_build": (ctypes.c_int, []),
+        "phg_field_packed": (S, [VP, ctypes.POINTER(VP), ctypes.POINTER(I64),
+                                 ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_float)]),
+        "phg_field_create_packed": (S, [ctypes.POINTER(VP), I64, I64, I64,
+                                        ctypes.POINTER(ctypes.c_double), ctypes.c_double,
+                                        ctypes.c_int32, ctypes.c_float, VP]),
+        "phg_field_packed_done": (S, [VP, VP]),
         "phg_field_from_oovl": (S, [ctypes.POINTER(VP), VP, VP, I64, I64, I64, I64,
                                     ctypes.POINTER(ctypes.c_double), ctypes.c_double, VP]),
     }

@@ -57,6 +57,50 @@ def exchange_counts(n_strands: int, n_verts: int, group=None, device="cpu") -> S
                      int(counts[:, 0].sum()), int(counts[:, 1].sum()))
 
 
+def replicate_field(vol=None, src=0, group=None, device="cuda"):
+    """The packed field on every rank from ONE rank's upload (multi-GPU setup).
+
+    Rank ``src`` packs ``vol`` (occ/ori host arrays) once; the padded float4 buffer (2 GiB at
+    512^3) and its geometry are broadcast to the other ranks -- NCCL over NVLink when
+    ``device`` is "cuda", staged through host memory for gloo ("cpu") -- so no other rank
+    reads or packs the host arrays.  Returns this rank's DeviceField (bit-identical buffers).
+    """
+    import torch
+    import torch.distributed as dist
+
+    from .phg import _CudaArray
+    from .volume import DeviceField
+
+    rank = dist.get_rank(group)
+    glob_src = dist.get_global_rank(group, src) if group is not None else src
+    f = None
+    meta = torch.zeros(9, dtype=torch.float64)
+    if rank == src:
+        f = DeviceField(vol.origin, vol.voxel_size, vol.occ, vol.ori)
+        _, _, zeroed, maxabs = f.packed()
+        meta[:] = torch.tensor([*f.dims, *f.origin.tolist(), f.voxel_size, float(zeroed),
+                                maxabs if np.isfinite(maxabs) else -1.0], dtype=torch.float64)
+    meta = meta.to(device)
+    dist.broadcast(meta, glob_src, group=group)
+    m = meta.cpu().tolist()
+    if rank != src:
+        f = DeviceField.create_packed([int(m[0]), int(m[1]), int(m[2])], m[3:6], m[6],
+                                      m[7] != 0.0, m[8] if m[8] >= 0 else float("inf"))
+    ptr, nbytes, _, _ = f.packed()
+    buf = torch.as_tensor(_CudaArray(ptr, (nbytes,), "|u1"), device=torch.cuda.current_device())
+    if str(device).startswith("cuda"):
+        dist.broadcast(buf, glob_src, group=group)
+    else:  # gloo: through host memory
+        host = buf.cpu() if rank == src else torch.empty(nbytes, dtype=torch.uint8)
+        dist.broadcast(host, glob_src, group=group)
+        if rank != src:
+            buf.copy_(host)
+    torch.cuda.synchronize()
+    if rank != src:
+        f.packed_done()
+    return f
+
+
 def exchange_counts_device(n_strands_t, n_verts_t, group=None, device="cpu"):
     """exchange_counts without a host synchronisation (NCCL): the (strands, vertices) pair is
     built from device tensors (e.g. phg_trace_rows' kept-vertex counter) and all-gathered on

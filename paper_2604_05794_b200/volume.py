@@ -141,6 +141,31 @@ class DeviceField:
         self._near_key = None
         return self
 
+    @classmethod
+    def create_packed(cls, dims, origin, voxel_size, zeroed, maxabs, stream=0):
+        """A field whose packed buffer the caller fills (dist.replicate_field); finish with
+        ``packed_done()``."""
+        lib = _native.load()
+        origin = np.ascontiguousarray(np.asarray(origin, dtype=np.float64).reshape(3))
+        h = ctypes.c_void_p()
+        _native.check(lib.phg_field_create_packed(
+            ctypes.byref(h), int(dims[0]), int(dims[1]), int(dims[2]),
+            origin.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), float(voxel_size),
+            int(bool(zeroed)), float(maxabs), stream), "phg_field_create_packed")
+        return cls.from_handle(h, dims, origin, voxel_size)
+
+    def packed(self):
+        """(device pointer, bytes, zeroed, maxabs) of the padded packed voxel buffer."""
+        ptr, nb = ctypes.c_void_p(), ctypes.c_int64()
+        z, m = ctypes.c_int32(), ctypes.c_float()
+        _native.check(self._lib.phg_field_packed(self.handle, ctypes.byref(ptr), ctypes.byref(nb),
+                                                 ctypes.byref(z), ctypes.byref(m)),
+                      "phg_field_packed")
+        return int(ptr.value or 0), int(nb.value), bool(z.value), float(m.value)
+
+    def packed_done(self, stream=0):
+        _native.check(self._lib.phg_field_packed_done(self.handle, stream), "phg_field_packed_done")
+
     def close(self):
         if self.handle:
             self._lib.phg_field_destroy(self.handle)

@@ -131,3 +131,39 @@ def test_two_rank_device_driver_equals_reference(tmp_path, name):
     assert np.array_equal(got["counts"], c.counts_out)
     assert np.array_equal(np.load(out + ".counts1.npy"), c.counts_out)  # replicas agree
     assert json.loads(str(got["report"])) == json.loads(str(c.report))
+
+
+def _replicate_worker(rank, world, port, case_path, out_path):
+    torch, dist = _init(rank, world, port)
+    try:
+        from paper_2604_05794_b200 import dist as pdist
+        from paper_2604_05794_b200 import phg
+
+        c = load_case(case_path)
+        f = pdist.replicate_field(c.vol if rank == 0 else None, src=0, device="cpu")
+        cap = getattr(c, "at_cap", None)
+        f.set_cap(cap if cap is not None and cap.any() else None)
+        off, v, e = phg.trace_device(f, torch.from_numpy(c.seeds).cuda(),
+                                     torch.from_numpy(c.dirs).cuda(), c.params)
+        ptr, nbytes, zeroed, maxabs = f.packed()
+        np.savez(out_path + f".{rank}.npz", offsets=off.cpu().numpy(), verts=v.cpu().numpy(),
+                 entered=e.cpu().numpy(), meta=np.array([nbytes, zeroed, maxabs]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("name", ["trace_sparse48", "trace_curly40_cap"])
+def test_field_replicated_from_one_rank(tmp_path, name):
+    """dist.replicate_field: rank 0 packs the field once and broadcasts the packed buffer;
+    rank 1, which never sees the host arrays, traces the reference fixture bit-exactly."""
+    path = os.path.join(GOLDEN, f"{name}.npz")
+    out = str(tmp_path / "out")
+    mp.start_processes(_replicate_worker, args=(2, _free_port(), path, out), nprocs=2,
+                       join=True, start_method="spawn")
+    c = load_case(path)
+    r0, r1 = np.load(out + ".0.npz"), np.load(out + ".1.npz")
+    assert np.array_equal(r0["meta"], r1["meta"])
+    for r in (r0, r1):
+        assert np.array_equal(r["offsets"], c.offsets)
+        assert np.array_equal(r["verts"], c.verts)
+        assert np.array_equal(r["entered"].astype(bool), c.entered)
