@@ -479,20 +479,7 @@ def run_ours(args):
     setup = None
     need_field = ws == 1 or rank == 0 or cfg.kind == "sparse"
     ori, occ = cfg.field(dev) if need_field else (None, None)
-    if ws == 1:
-        field = DeviceField(np.zeros(3), synth.VOXEL_MM, occ, ori,
-                            torch.cuda.current_stream(dev).cuda_stream)
-    else:
-        from types import SimpleNamespace
-
-        src = SimpleNamespace(origin=np.zeros(3), voxel_size=synth.VOXEL_MM, occ=occ, ori=ori)
-        dist.barrier()
-        t0 = time.perf_counter()
-        field = pdist.replicate_field(src if rank == 0 else None, src=0, device=coll)
-        dist.barrier()
-        setup = {"field_replicate_s": time.perf_counter() - t0,
-                 "field_bytes": field.packed()[1],
-                 "how": "rank 0 packs, dist.replicate_field broadcasts the packed buffer"}
+    torch.cuda.empty_cache()  # the generator's temporaries (the C5 smoothing: tens of GB)
     ori_host = occ_host = None
     if ws == 1 and not args.no_cpu:
         ori_host, occ_host = ori.cpu().numpy(), occ.cpu().numpy()
@@ -501,6 +488,23 @@ def run_ours(args):
     if ori_host is not None:  # C1 all seeds, C2-C5 the first 16384
         k = min(args.cpu_sample or (cfg.seeds if cfg.name == "C1" else CPU_SUBSET), len(all_seeds))
         cpu_seeds = (np.ascontiguousarray(all_seeds[:k]), np.ascontiguousarray(all_dirs[:k]))
+    if ws == 1:
+        field = DeviceField(np.zeros(3), synth.VOXEL_MM, occ, ori,
+                            torch.cuda.current_stream(dev).cuda_stream)
+    else:
+        from types import SimpleNamespace
+
+        if rank != 0:  # only rank 0's copy feeds the field
+            ori = occ = None
+            torch.cuda.empty_cache()
+        src = SimpleNamespace(origin=np.zeros(3), voxel_size=synth.VOXEL_MM, occ=occ, ori=ori)
+        dist.barrier()
+        t0 = time.perf_counter()
+        field = pdist.replicate_field(src if rank == 0 else None, src=0, device=coll)
+        dist.barrier()
+        setup = {"field_replicate_s": time.perf_counter() - t0,
+                 "field_bytes": field.packed()[1],
+                 "how": "rank 0 packs, dist.replicate_field broadcasts the packed buffer"}
     del ori, occ
     torch.cuda.empty_cache()
 
