@@ -316,6 +316,23 @@ def run_reference(args):
     finally:
         pool.close()
     v = tot_s / tot_t
+    # BASELINE.md 2's other CPU legs, once (not per step): the reference's own multi-core
+    # path init_guide_strands(workers=W, field_seeds=0) and trace_batch on one core
+    extra = {}
+    if not args.no_cpu:
+        counts = np.zeros(occ.shape, np.uint16)
+        t0 = time.perf_counter()
+        segs, st = onp.init_guide_strands_scalp(f, counts, seeds, dirs, params, cores)
+        dt = time.perf_counter() - t0
+        extra["init_guide_strands"] = {
+            "value": st / dt, "seconds": dt, "segments": len(segs),
+            "what": f"port of init_guide_strands(workers={cores}, field_seeds=0) as strandkit "
+                    "bench times it (cli.py:233-237): pool made per call, serial commit loop"}
+        t0 = time.perf_counter()
+        _, keep, _ = onp.trace(f, seeds, dirs, params)
+        dt = time.perf_counter() - t0
+        extra["one_core"] = {"value": int((keep - 1).sum()) / dt, "seconds": dt,
+                             "what": "trace_batch port in one process (BASELINE.md 2 (i))"}
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": v, "unit": "steps/s", "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps,
@@ -329,7 +346,7 @@ def run_reference(args):
                                    f"restatement of trace_batch (pinned bit-exact to the "
                                    f"reference) in a persistent {cores}-process fork pool, "
                                    f"{len(seeds) // cores} seeds per worker (phg.py:184-207 "
-                                   f"slicing); host {model}"},
+                                   f"slicing); host {model}", **extra},
         "e2e": {"value": v, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 

@@ -34,6 +34,7 @@ def test_reference_arm_line():
     cb = d["cpu_baseline"]
     assert {"value", "unit", "cores", "kind", "sample"} <= set(cb) and cb["kind"] == "port"
     assert cb["value"] == d["value"] and d["e2e"]["value"] == d["value"]
+    assert cb["init_guide_strands"]["value"] > 0 and cb["one_core"]["value"] > 0
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
 
 
