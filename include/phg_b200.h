@@ -141,7 +141,7 @@ phg_status phg_trace_rows(phg_ctx* c, const phg_field* f, const phg_params_v1* p
                           phg_rows_v1* out, void* stream);
 
 /* End-to-end variant of phg_trace + phg_gather for HOST seeds and HOST outputs: seeds are
- * traced in chunks of `chunk` (<= 0: n/4, at least 65536) and the D2H copy of chunk k's
+ * traced in chunks of `chunk` (<= 0: n/8, at least 131072) and the D2H copy of chunk k's
  * vertices (on an internal copy stream) overlaps the device work of chunk k+1.  offsets
  * (n+1) i64, entered (n) u8, verts (verts_cap,3) f64: pinned host memory gives the overlap.
  * Relaxed mode only (strict mode couples all seeds per step).  If the vertices exceed
