@@ -107,3 +107,49 @@ def test_device_count_exchange_matches_host_exchange(tmp_path):
     got = np.load(out)
     assert np.array_equal(got["dev"], [[10, 100], [11, 200]])
     assert np.array_equal(got["dev"], got["host"])
+
+
+def _uneven_worker(rank, world, port, case_path, n, out_path):
+    import sys
+
+    sys.path.insert(0, ROOT)
+    import torch.distributed as dist
+
+    from oracle import phg_oracle_c as oc
+    from paper_2604_05794_b200 import dist as pdist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        c = load_case(case_path)
+
+        def trace_fn(pos, dirs):
+            slab, keep, ent = oc.trace(c.origin, c.voxel_size, c.occ, c.ori, pos, dirs, c.params)
+            off, v = oc.to_csr(slab, keep)
+            return off, v, ent
+
+        off_g, verts, ent, info = pdist.trace_sharded(trace_fn, c.seeds[:n], c.dirs[:n])
+        res = pdist.gather_to_root(off_g[:-1], verts, ent, info)
+        if rank == 0:
+            off, v, e = res
+            np.savez(out_path, offsets=off, verts=v, entered=e, counts=info.counts)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n", [2, 5])
+def test_ranks_without_seeds_gather_cleanly(tmp_path, n, oracle_c):
+    """More ranks than seeds (some ranks trace nothing): the point-to-point gather skips the
+    empty payloads and root still reassembles the single-process CSR byte for byte."""
+    path = os.path.join(GOLDEN, "trace_sparse48.npz")
+    out = str(tmp_path / "out.npz")
+    mp.start_processes(_uneven_worker, args=(3, _free_port(), path, n, out), nprocs=3,
+                       join=True, start_method="spawn")
+    got = np.load(out)
+    c = load_case(path)
+    slab, keep, ent = oracle_c.trace(c.origin, c.voxel_size, c.occ, c.ori, c.seeds[:n],
+                                     c.dirs[:n], c.params)
+    off, v = oracle_c.to_csr(slab, keep)
+    assert np.array_equal(got["offsets"], off) and np.array_equal(got["verts"], v)
+    assert np.array_equal(got["entered"], ent)
+    assert (got["counts"][:, 0] == 0).any() or n >= 3
