@@ -727,3 +727,24 @@ def test_fuzz_sampler_and_trace_bit_exact(gpu, oracle_c, seed):
         slab, keep, ent_o = oracle_c.trace(origin, vs, occ, ori, seeds, dirs, p, at_cap=cap)
         off_o, v_o = oracle_c.to_csr(slab, keep)
         assert np.array_equal(off, off_o) and np.array_equal(v, v_o) and np.array_equal(ent, ent_o)
+
+
+def test_steering_runs_on_the_fast_sampler(gpu, oracle_c):
+    """Steering (near_occ, steer > 0, phg.py:108-117) on a finite field now samples with the
+    fast (zeroed-field) sampler; it equals the C oracle bit for bit, with and without a cap
+    plane."""
+    from scipy.ndimage import distance_transform_edt
+
+    vol, s, d, p = _config_case("sparse", 64, 4_000, 71, interior=1_000)
+    _, inds = distance_transform_edt(~vol.occ, return_indices=True)
+    near = np.ascontiguousarray(np.stack(inds, axis=-1).astype(np.int64))
+    p = SimpleNamespace(**vars(p))
+    p.steer = 0.35
+    for cap in (None, np.random.default_rng(4).random(vol.occ.shape) < 0.02):
+        off, v, ent = gpu.phg.trace_batch_csr(vol, s, d, p, at_cap=cap, near_occ=near)
+        assert gpu.phg._tracer().last_sampler() == "fast-pow2"
+        slab, keep, ent_o = oracle_c.trace(vol.origin, vol.voxel_size, vol.occ, vol.ori, s, d, p,
+                                           at_cap=cap, near_occ=near)
+        off_o, v_o = oracle_c.to_csr(slab, keep)
+        assert np.array_equal(off, off_o) and np.array_equal(v, v_o)
+        assert np.array_equal(ent, ent_o)
