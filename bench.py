@@ -48,6 +48,8 @@ def parse():
                          "device: code-path validation only, not a scaling measurement)")
     ap.add_argument("--seeds", type=int, default=0, help="override seeds per rank")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-root-gather", action="store_true",
+                    help="N > 1: skip the peer-memory gather of every rank's CSR to rank 0")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=0, help="seeds in the CPU sample")
     ap.add_argument("--sweep", action="store_true", help="time every trace-kernel variant")
@@ -620,6 +622,13 @@ def run_ours(args):
         e2e = e2e_leg(args, tracer, field, params, s_host, d_host, per_rank, ws, coll,
                       total_steps)
 
+    # N > 1: the rank-order concatenation on rank 0, fused into each rank's CSR gather kernel
+    # writing over peer memory (dist.gather_csr_to_root_p2p; NVLink between GPUs)
+    root_gather = None
+    if ws > 1 and not args.no_root_gather:
+        root_gather = root_gather_leg(args, tracer, field, params, s_dev, d_dev, per_rank, stream,
+                                      coll)
+
     # the remaining legs run on their own contexts: release the timed context's slab and CSR
     # scratch first (C4's 4M seeds hold ~77 GB there)
     tracer.close()
@@ -659,7 +668,7 @@ def run_ours(args):
             "value_csr": value_csr, "ms_per_step_csr": ms_csr,
             "roofline": roofline_block(cfg, accepted, kernel_ms),
             "cpu_baseline": cpu, "e2e": e2e, "clocks": clk, "driver": driver, "a9": a9,
-            "dropin": dropin, "setup": setup,
+            "dropin": dropin, "setup": setup, "root_gather": root_gather,
             "gpu_launches": args.steps * phg.LAUNCHES_PER_TRACE_ROWS,
         }
         if shared:
@@ -668,6 +677,37 @@ def run_ours(args):
         print(json.dumps(line), flush=True)
     if ws > 1:
         dist.destroy_process_group()
+
+
+def root_gather_leg(args, tracer, field, params, s_dev, d_dev, per_rank, stream, coll):
+    """Every rank's CSR written straight into rank 0's global CSR by its own gather kernel over
+    peer memory (CUDA IPC; NVLink P2P between GPUs): time from the first barrier to the last,
+    max over ranks (not part of the timed region of `value`)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2604_05794_b200 import dist as pdist
+
+    off = torch.empty(per_rank + 1, dtype=torch.int64, device=s_dev.device)
+    ent = torch.empty(max(per_rank, 1), dtype=torch.uint8, device=s_dev.device)
+    m = tracer.trace(field, params, s_dev.data_ptr(), d_dev.data_ptr(), per_rank,
+                     off.data_ptr(), ent.data_ptr(), None, stream.cuda_stream)
+    info = pdist.exchange_counts(per_rank, m, device=coll)
+    try:
+        dist.barrier()
+        t0 = time.perf_counter()
+        res = pdist.gather_csr_to_root_p2p(tracer, info, return_result=False)
+        dt = time.perf_counter() - t0
+    except Exception as exc:  # noqa: BLE001 - IPC may be unavailable on some hosts
+        return {"error": str(exc).splitlines()[0][:200]}
+    t = torch.tensor([dt], dtype=torch.float64, device=coll)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dt = float(t.item())
+    if res is None:
+        return None
+    return {"seconds": dt, "bytes": res["bytes"], "gbs": res["bytes"] / dt / 1e9,
+            "what": "dist.gather_csr_to_root_p2p: rank-order CSR on rank 0, each rank's gather "
+                    "kernel writing into it over peer memory (IPC handles, NVLink P2P)"}
 
 
 def driver_leg(cfg, field, s_host, d_host, dev, repeats=2):

@@ -152,6 +152,23 @@ phg_status phg_trace_to_host(phg_ctx* c, const phg_field* f, const phg_params_v1
                              int64_t chunk, int64_t* offsets, uint8_t* entered, double* verts,
                              int64_t verts_cap, int64_t* n_verts_out, void* stream);
 
+/* ---- rank-order concatenation on one GPU over peer memory (multi-GPU) -------
+ * The CSR gather of the last phg_trace, fused with the concatenation on the root GPU: the
+ * gather kernel writes this rank's strands straight into the root's global CSR (peer memory
+ * over NVLink, opened with phg_ipc_open) at the rank's global bases, so the "gather to root"
+ * collective costs no separate copy.
+ * phg_gather_to: verts/offsets/entered are the GLOBAL buffers ((M,3) f64, (N+1) i64, (N) u8,
+ *   device or peer memory); vert_base / strand_base this rank's place in them (exclusive
+ *   sums of the ranks before it).  Enqueued on `stream`.
+ * phg_ipc_alloc / phg_ipc_free: a device buffer whose CUDA IPC handle (64 bytes) other
+ *   processes open with phg_ipc_open (a device pointer to the same memory; phg_ipc_close). */
+phg_status phg_gather_to(phg_ctx* c, double* verts, int64_t* offsets, uint8_t* entered,
+                         int64_t vert_base, int64_t strand_base, void* stream);
+phg_status phg_ipc_alloc(int64_t bytes, void** dev_ptr, uint8_t handle[64]);
+phg_status phg_ipc_free(void* dev_ptr);
+phg_status phg_ipc_open(const uint8_t handle[64], void** dev_ptr);
+phg_status phg_ipc_close(void* dev_ptr);
+
 /* Checked build only (libphg_b200_checked.so, compiled with PHG_CHECKED; the stand-in for
  * compute-sanitizer): waits for the device, then reports device-side index-check violations
  * of the hot kernels (with the first failing check's site id) and the number of live library

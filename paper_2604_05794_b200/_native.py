@@ -40,7 +40,8 @@ EXPORTS = (
     "phg_grow_begin", "phg_grow_scalp_batch", "phg_grow_field_begin", "phg_grow_field_batch",
     "phg_grow_commits", "phg_grow_apply", "phg_grow_end", "phg_trace_rows",
     "phg_debug_checks", "phg_is_checked_build", "phg_field_packed", "phg_field_create_packed",
-    "phg_field_packed_done",
+    "phg_field_packed_done", "phg_gather_to", "phg_ipc_alloc", "phg_ipc_free", "phg_ipc_open",
+    "phg_ipc_close",
 )
 
 
@@ -137,6 +138,11 @@ def _declare(lib):
                                         ctypes.POINTER(ctypes.c_double), ctypes.c_double,
                                         ctypes.c_int32, ctypes.c_float, VP]),
         "phg_field_packed_done": (S, [VP, VP]),
+        "phg_gather_to": (S, [VP, VP, VP, VP, I64, I64, VP]),
+        "phg_ipc_alloc": (S, [I64, ctypes.POINTER(VP), VP]),
+        "phg_ipc_free": (S, [VP]),
+        "phg_ipc_open": (S, [VP, ctypes.POINTER(VP)]),
+        "phg_ipc_close": (S, [VP]),
         "phg_field_from_oovl": (S, [ctypes.POINTER(VP), VP, VP, I64, I64, I64, I64,
                                     ctypes.POINTER(ctypes.c_double), ctypes.c_double, VP]),
     }

@@ -286,6 +286,83 @@ def init_guide_strands_multirank(seeds, normals, counts, params, backend, group=
     return offsets_all, verts_all, rooted_all, report
 
 
+def gather_csr_to_root_p2p(tracer, info: ShardInfo, group=None, root=0, return_result=True):
+    """The CSR of the last ``tracer.trace`` on every rank, concatenated in rank order on
+    ``root``'s GPU by the gather kernel itself: root allocates the global CSR once
+    (``phg_ipc_alloc``), every rank opens it as peer memory (CUDA IPC; NVLink P2P between GPUs)
+    and ``phg_gather_to`` writes the rank's strands straight to their global places -- the
+    gather and the "gather to root" collective are one kernel per rank, no NCCL payload
+    transfer.  ``info`` is this rank's ``exchange_counts`` result.
+
+    Returns (offsets (N+1,), verts (M,3), entered (N,)) as CUDA tensors on root, None elsewhere
+    (``return_result=False``: the global buffers are freed after the gather, root returns
+    their sizes -- the measurement leg of bench.py).
+    """
+    import ctypes
+
+    import torch
+    import torch.distributed as dist
+
+    from . import _native
+    from .phg import _CudaArray
+
+    lib = _native.load()
+    rank = dist.get_rank(group)
+    glob_root = dist.get_global_rank(group, root) if group is not None else root
+    N, M = int(info.n_strands), int(info.n_verts)
+    sizes = (M * 24, (N + 1) * 8, max(N, 1))
+    handles = torch.zeros(3 * 64, dtype=torch.uint8)
+    ptrs = [None] * 3
+    if rank == root:
+        for k, nb in enumerate(sizes):
+            p, hb = ctypes.c_void_p(), ctypes.create_string_buffer(64)
+            _native.check(lib.phg_ipc_alloc(nb, ctypes.byref(p), ctypes.cast(hb, ctypes.c_void_p)),
+                          "phg_ipc_alloc")
+            ptrs[k] = p.value
+            handles[64 * k: 64 * (k + 1)] = torch.frombuffer(bytearray(hb.raw), dtype=torch.uint8)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    bcast_dev = "cpu" if dist.get_backend(group) == "gloo" else dev
+    h = handles.to(bcast_dev)
+    dist.broadcast(h, glob_root, group=group)
+    opened = []
+    try:
+        if rank != root:
+            raw = bytes(h.cpu().numpy().tobytes())
+            for k in range(3):
+                p = ctypes.c_void_p()
+                hb = ctypes.create_string_buffer(raw[64 * k: 64 * (k + 1)], 64)
+                _native.check(lib.phg_ipc_open(ctypes.cast(hb, ctypes.c_void_p), ctypes.byref(p)),
+                              "phg_ipc_open")
+                ptrs[k] = p.value
+                opened.append(p.value)
+        _native.check(lib.phg_gather_to(tracer.handle, ptrs[0], ptrs[1], ptrs[2],
+                                        int(info.vert_start), int(info.strand_start), 0),
+                      "phg_gather_to")
+        torch.cuda.synchronize()
+        dist.barrier(group=group)  # every rank's strands are in place
+    finally:
+        for p in opened:
+            lib.phg_ipc_close(p)
+    if rank != root:
+        return None
+    if not return_result:
+        for p in ptrs:
+            lib.phg_ipc_free(p)
+        return {"strands": N, "vertices": M, "bytes": int(sum(sizes))}
+    try:
+        off = torch.as_tensor(_CudaArray(ptrs[1], (N + 1,), "<i8"), device=dev).clone()
+        off[N] = M
+        verts = (torch.as_tensor(_CudaArray(ptrs[0], (M, 3), "<f8"), device=dev).clone()
+                 if M else torch.empty((0, 3), dtype=torch.float64, device=dev))
+        ent = (torch.as_tensor(_CudaArray(ptrs[2], (N,), "|u1"), device=dev).clone()
+               if N else torch.empty(0, dtype=torch.uint8, device=dev))
+        torch.cuda.synchronize()
+    finally:
+        for p in ptrs:
+            lib.phg_ipc_free(p)
+    return off, verts, ent
+
+
 def gather_to_root(offsets_global, verts, entered, info: ShardInfo, group=None, device="cpu",
                    root=0):
     """Concatenate every rank's CSR on ``root``: each rank sends its payload straight to root
