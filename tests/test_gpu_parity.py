@@ -748,44 +748,3 @@ def test_steering_runs_on_the_fast_sampler(gpu, oracle_c):
         off_o, v_o = oracle_c.to_csr(slab, keep)
         assert np.array_equal(off, off_o) and np.array_equal(v, v_o)
         assert np.array_equal(ent, ent_o)
-
-
-@pytest.mark.parametrize("kind,n,dims", [("sparse", 64, None), ("sparse", 40, (37, 41, 43)),
-                                         ("curly", 48, None)])
-def test_empty_space_fast_forward_bit_exact(gpu, oracle_c, monkeypatch, kind, n, dims):
-    """Empty-space fast-forward (steps whose two samples lie in clear bricks skip the sampler:
-    exactly (0, has=False, support=+0)) equals the oracle bit for bit: probing and coasting
-    strands, the cap plane, odd dims, strands leaving the grid, max_vertices cut-offs."""
-    vol, s, d, p = _config_case(kind, n, 5_000, 81, interior=2_000 if kind == "sparse" else 0)
-    if dims is not None:
-        vol.occ = np.ascontiguousarray(vol.occ[: dims[0], : dims[1], : dims[2]])
-        vol.ori = np.ascontiguousarray(vol.ori[: dims[0], : dims[1], : dims[2]])
-        vol.dims = vol.occ.shape
-    monkeypatch.setenv("PHG_FF", "1")
-    gpu.volume.invalidate()
-    tr = gpu.phg._tracer()
-    cap = np.random.default_rng(11).random(vol.occ.shape) < 0.02
-    for plane in (None, cap):
-        for pp in (p, SimpleNamespace(**{**vars(p), "max_vertices": 37, "probe_steps": 40})):
-            off, v, ent = gpu.phg.trace_batch_csr(vol, s, d, pp, at_cap=plane)
-            assert tr.last_variant() == "default+fast-forward", tr.last_variant()
-            slab, keep, ent_o = oracle_c.trace(vol.origin, vol.voxel_size, vol.occ, vol.ori, s, d,
-                                               pp, at_cap=plane)
-            off_o, v_o = oracle_c.to_csr(slab, keep)
-            assert np.array_equal(off, off_o) and np.array_equal(v, v_o)
-            assert np.array_equal(ent, ent_o)
-    # min_support <= 0 keeps the plain kernel (an empty sample would count as supported)
-    gpu.phg.trace_batch_csr(vol, s[:100], d[:100], SimpleNamespace(**{**vars(p), "min_support": 0.0}))
-    assert tr.last_variant() != "default+fast-forward"
-    gpu.volume.invalidate()
-
-
-def test_fast_forward_chosen_for_sparse_fields(gpu, monkeypatch):
-    """Without PHG_FF the fast-forward kernels run on fields with >= 50% clear bricks (C5-like
-    sparse), not on dense ones (C3's cylinder)."""
-    monkeypatch.delenv("PHG_FF", raising=False)
-    tr = gpu.phg._tracer()
-    for kind, want in (("sparse", True), ("curly", False)):
-        vol, s, d, p = _config_case(kind, 64, 200, 91)
-        gpu.phg.trace_batch_csr(vol, s, d, p)
-        assert (tr.last_variant() == "default+fast-forward") == want, (kind, tr.last_variant())
