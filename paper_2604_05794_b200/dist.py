@@ -311,23 +311,37 @@ def gather_csr_to_root_p2p(tracer, info: ShardInfo, group=None, root=0, return_r
     glob_root = dist.get_global_rank(group, root) if group is not None else root
     N, M = int(info.n_strands), int(info.n_verts)
     sizes = (M * 24, (N + 1) * 8, max(N, 1))
-    handles = torch.zeros(3 * 64, dtype=torch.uint8)
+    handles = torch.zeros(3 * 64 + 1, dtype=torch.uint8)  # + status byte: 1 = root allocated
     ptrs = [None] * 3
+    err = None
     if rank == root:
-        for k, nb in enumerate(sizes):
-            p, hb = ctypes.c_void_p(), ctypes.create_string_buffer(64)
-            _native.check(lib.phg_ipc_alloc(nb, ctypes.byref(p), ctypes.cast(hb, ctypes.c_void_p)),
-                          "phg_ipc_alloc")
-            ptrs[k] = p.value
-            handles[64 * k: 64 * (k + 1)] = torch.frombuffer(bytearray(hb.raw), dtype=torch.uint8)
+        try:
+            for k, nb in enumerate(sizes):
+                p, hb = ctypes.c_void_p(), ctypes.create_string_buffer(64)
+                _native.check(lib.phg_ipc_alloc(nb, ctypes.byref(p),
+                                                ctypes.cast(hb, ctypes.c_void_p)), "phg_ipc_alloc")
+                ptrs[k] = p.value
+                handles[64 * k: 64 * (k + 1)] = torch.frombuffer(bytearray(hb.raw),
+                                                                 dtype=torch.uint8)
+            handles[-1] = 1
+        except Exception as exc:  # noqa: BLE001 - every rank must learn it before going on
+            err = exc
+            for q in ptrs:
+                if q:
+                    lib.phg_ipc_free(q)
     dev = torch.device("cuda", torch.cuda.current_device())
     bcast_dev = "cpu" if dist.get_backend(group) == "gloo" else dev
     h = handles.to(bcast_dev)
     dist.broadcast(h, glob_root, group=group)
+    if int(h[-1].item()) != 1:
+        from .errors import PipelineError
+
+        raise PipelineError(f"gather_csr_to_root_p2p: the root could not allocate the global CSR "
+                            f"({err if err is not None else 'see the root rank'})")
     opened = []
     try:
         if rank != root:
-            raw = bytes(h.cpu().numpy().tobytes())
+            raw = bytes(h[:-1].cpu().numpy().tobytes())
             for k in range(3):
                 p = ctypes.c_void_p()
                 hb = ctypes.create_string_buffer(raw[64 * k: 64 * (k + 1)], 64)
