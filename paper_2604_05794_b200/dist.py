@@ -339,6 +339,7 @@ def gather_csr_to_root_p2p(tracer, info: ShardInfo, group=None, root=0, return_r
         raise PipelineError(f"gather_csr_to_root_p2p: the root could not allocate the global CSR "
                             f"({err if err is not None else 'see the root rank'})")
     opened = []
+    err = None
     try:
         if rank != root:
             raw = bytes(h[:-1].cpu().numpy().tobytes())
@@ -353,10 +354,21 @@ def gather_csr_to_root_p2p(tracer, info: ShardInfo, group=None, root=0, return_r
                                         int(info.vert_start), int(info.strand_start), 0),
                       "phg_gather_to")
         torch.cuda.synchronize()
-        dist.barrier(group=group)  # every rank's strands are in place
+    except Exception as exc:  # noqa: BLE001 - reported to every rank below
+        err = exc
     finally:
         for p in opened:
             lib.phg_ipc_close(p)
+    # every rank's strands are in place -- or every rank learns that one failed
+    ok = torch.tensor([0 if err else 1], dtype=torch.int32, device=bcast_dev)
+    dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=group)
+    if not int(ok.item()):
+        if rank == root:
+            for p in ptrs:
+                lib.phg_ipc_free(p)
+        from .errors import PipelineError
+
+        raise PipelineError(f"gather_csr_to_root_p2p failed on a rank ({err or 'another rank'})")
     if rank != root:
         return None
     if not return_result:
