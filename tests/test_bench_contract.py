@@ -54,3 +54,24 @@ def test_our_arm_line():
     assert d["clocks"] and d["clocks"]["samples"] > 0 and "reasons" in d["clocks"]
     assert d["gpu_launches"] == 3 * 8
     assert d["steps_per_trace"] == 1_260_000  # C1: 10k strands x 126 returned steps
+
+
+def test_reference_arm_under_torchrun_prints_one_line():
+    """The driver launches the reference arm like ours at N > 1 (torchrun); rank 0 alone runs
+    it and prints ONE line, the other ranks exit 0 without work."""
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                        "--nproc-per-node", "2", "--master-addr", "127.0.0.1", "--master-port",
+                        str(port), os.path.join(ROOT, "bench.py"), "--impl", "reference",
+                        "--gpus", "2", "--config", "C1", "--steps", "1", "--warmup", "1",
+                        "--cpu-sample", "300", "--no-cpu"], cwd=ROOT, capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.strip().splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
