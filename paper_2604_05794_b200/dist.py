@@ -9,11 +9,13 @@ reference's own fork-pool split, ``np.linspace(0, n, world + 1)``
 single-GPU CSR byte for byte -- the analogue of the reference's
 "identical output for any worker count" contract (A9, test_acceptance.py:326).
 
-The only communication is one all-gather of per-rank (strands, vertices)
-counts, from which every rank derives its global CSR offsets; payloads stay
-rank-local unless ``gather_to_root`` is asked for, which moves each rank's payload
-to the root only (point-to-point), never to every rank.  The same code runs over
-NCCL (CUDA tensors) and gloo (CPU tensors, used by the CPU tests).
+The only communication on the trace path is one all-gather of per-rank (strands,
+vertices) counts, from which every rank derives its global CSR offsets; payloads stay
+rank-local unless asked for: ``gather_to_root`` moves each rank's payload to the root only
+(point-to-point), never to every rank, and ``gather_csr_to_root_p2p`` has each rank's CSR
+gather kernel write straight into the root's global CSR over peer memory.  Setup:
+``replicate_field`` packs the field once and broadcasts the packed buffer.  The same code
+runs over NCCL (CUDA tensors) and gloo (CPU tensors, used by the CPU tests).
 """
 
 from __future__ import annotations
@@ -74,15 +76,26 @@ def replicate_field(vol=None, src=0, group=None, device="cuda"):
     rank = dist.get_rank(group)
     glob_src = dist.get_global_rank(group, src) if group is not None else src
     f = None
-    meta = torch.zeros(9, dtype=torch.float64)
+    err = None
+    meta = torch.zeros(9, dtype=torch.float64)  # dims[0] = -1: the source could not pack it
     if rank == src:
-        f = DeviceField(vol.origin, vol.voxel_size, vol.occ, vol.ori)
-        _, _, zeroed, maxabs = f.packed()
-        meta[:] = torch.tensor([*f.dims, *f.origin.tolist(), f.voxel_size, float(zeroed),
-                                maxabs if np.isfinite(maxabs) else -1.0], dtype=torch.float64)
+        try:
+            f = DeviceField(vol.origin, vol.voxel_size, vol.occ, vol.ori)
+            _, _, zeroed, maxabs = f.packed()
+            meta[:] = torch.tensor([*f.dims, *f.origin.tolist(), f.voxel_size, float(zeroed),
+                                    maxabs if np.isfinite(maxabs) else -1.0],
+                                   dtype=torch.float64)
+        except Exception as exc:  # noqa: BLE001 - every rank must learn it before going on
+            err = exc
+            meta[0] = -1.0
     meta = meta.to(device)
     dist.broadcast(meta, glob_src, group=group)
     m = meta.cpu().tolist()
+    if m[0] < 0:
+        from .errors import PipelineError
+
+        raise PipelineError(f"replicate_field: the source rank could not pack the field "
+                            f"({err if err is not None else 'see the source rank'})")
     if rank != src:
         f = DeviceField.create_packed([int(m[0]), int(m[1]), int(m[2])], m[3:6], m[6],
                                       m[7] != 0.0, m[8] if m[8] >= 0 else float("inf"))
