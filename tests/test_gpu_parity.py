@@ -748,3 +748,27 @@ def test_steering_runs_on_the_fast_sampler(gpu, oracle_c):
         off_o, v_o = oracle_c.to_csr(slab, keep)
         assert np.array_equal(off, off_o) and np.array_equal(v, v_o)
         assert np.array_equal(ent, ent_o)
+
+
+def test_rows_api_edge_cases(gpu):
+    """phg_trace_rows: zero seeds give an empty RowSet; strict mode (which needs live_counts
+    and per-step commits) is refused with the reference's DataError."""
+    torch = gpu.torch
+    from paper_2604_05794_b200.errors import DataError
+
+    vol, s, d, p = _config_case("curly", 32, 100, 97)
+    f = gpu.volume.field_for(vol)
+    f.set_cap(None)
+    f.set_near(None)
+    tr = gpu.phg.Tracer()
+    empty = torch.zeros((0, 3), dtype=torch.float64, device="cuda")
+    rs = gpu.phg.trace_device_rows(f, empty, empty, p, tracer=tr)
+    assert rs.n == 0 and rs.steps == 0 and rs.kept == 0
+    off, v, e = rs.to_csr()
+    assert off.shape == (1,) and v.shape == (0, 3) and e.shape == (0,)
+    ps = SimpleNamespace(**vars(p))
+    ps.strict = True
+    with pytest.raises(DataError):
+        gpu.phg.trace_device_rows(f, torch.from_numpy(s).cuda(), torch.from_numpy(d).cuda(), ps,
+                                  tracer=tr)
+    tr.close()
