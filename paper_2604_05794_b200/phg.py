@@ -358,7 +358,7 @@ class RowSet:
         seg = torch.repeat_interleave(torch.arange(self.n, device=self.rows.device),
                                       self.lengths)
         j = torch.arange(int(off[-1]), device=self.rows.device) - off[seg]
-        r3 = self.rows.view(self.rows.shape[0], -1, 3)
+        r3 = self.rows.view(self.rows.shape[0], self.row_stride // 3, 3)
         return off, r3[rows[seg], j], self.entered
 
 
