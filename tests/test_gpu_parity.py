@@ -644,14 +644,15 @@ def test_bricked_driver_bit_exact(gpu, monkeypatch):
     gpu.volume.invalidate()
 
 
-@pytest.mark.parametrize("kind", ["sparse", "curly"])
-def test_strict_cooperative_equals_per_step_launches(gpu, oracle_c, monkeypatch, kind):
+@pytest.mark.parametrize("kind,turn", [("sparse", 0.0), ("curly", 0.0), ("curly", 3.0)])
+def test_strict_cooperative_equals_per_step_launches(gpu, oracle_c, monkeypatch, kind, turn):
     """Strict mode in one cooperative launch (grid barriers between each step and its
     commits, early exit) equals the per-step launch pairs and the C oracle bit for bit,
     including the in-place live_counts (phg.py:136-155)."""
     vol, s, d, p = _config_case(kind, 48, 3_000, 61, interior=800 if kind == "sparse" else 0)
     p = SimpleNamespace(**vars(p))
     p.strict = True
+    p.max_turn_deg = turn  # the opt-in angle stop inside strict mode too
     outs = []
     for coop in ("1", "0"):
         monkeypatch.setenv("PHG_STRICT_COOP", coop)
