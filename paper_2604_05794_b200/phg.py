@@ -263,6 +263,24 @@ def split_rows(verts, offsets):
     return list(map(verts.__getitem__, map(slice, o[:-1], o[1:])))
 
 
+def _device_seeds(seed_pos, seed_dir):
+    """(n,3) float64 CUDA tensors, C-contiguous (the C ABI reads them as plain arrays)."""
+    import torch
+
+    out = []
+    for name, t in (("seed_pos", seed_pos), ("seed_dir", seed_dir)):
+        if not (torch.is_tensor(t) and t.is_cuda):
+            raise DataError(f"{name} must be a CUDA tensor")
+        if t.dtype != torch.float64:
+            raise DataError(f"{name} must be float64 (got {t.dtype})")
+        t = t.reshape(-1, 3).contiguous()
+        out.append(t)
+    if out[0].shape[0] != out[1].shape[0]:
+        raise DataError(f"seed_pos ({out[0].shape[0]}) and seed_dir ({out[1].shape[0]}) "
+                        "lengths differ")
+    return out[0], out[1]
+
+
 def trace_device(field, seed_pos, seed_dir, params, tracer=None, stream=None, order=True):
     """Zero-copy device API: torch CUDA tensors in, torch CUDA tensors out.
 
@@ -273,6 +291,7 @@ def trace_device(field, seed_pos, seed_dir, params, tracer=None, stream=None, or
     import torch
 
     tr = tracer or _tracer()
+    seed_pos, seed_dir = _device_seeds(seed_pos, seed_dir)
     n = int(seed_pos.shape[0])
     dev = seed_pos.device
     st = stream if stream is not None else torch.cuda.current_stream(dev)
@@ -369,6 +388,7 @@ def trace_device_rows(field, seed_pos, seed_dir, params, tracer=None, stream=Non
     import torch
 
     tr = tracer or _tracer()
+    seed_pos, seed_dir = _device_seeds(seed_pos, seed_dir)
     n = int(seed_pos.shape[0])
     dev = seed_pos.device
     st = stream if stream is not None else torch.cuda.current_stream(dev)

@@ -773,3 +773,27 @@ def test_rows_api_edge_cases(gpu):
         gpu.phg.trace_device_rows(f, torch.from_numpy(s).cuda(), torch.from_numpy(d).cuda(), ps,
                                   tracer=tr)
     tr.close()
+
+
+def test_device_api_validates_and_copies_strided_seeds(gpu):
+    """The device APIs take any (n,3) float64 CUDA tensors: strided views are made contiguous
+    (the C ABI reads plain arrays); wrong dtypes / lengths raise the reference's DataError."""
+    torch = gpu.torch
+    from paper_2604_05794_b200.errors import DataError
+
+    vol, s, d, p = _config_case("curly", 32, 400, 99)
+    f = gpu.volume.field_for(vol)
+    f.set_cap(None)
+    f.set_near(None)
+    sp, sd = torch.from_numpy(s).cuda(), torch.from_numpy(d).cuda()
+    ref = gpu.phg.trace_device(f, sp[::2], sd[::2], p)
+    got = gpu.phg.trace_device(f, sp[::2].contiguous(), sd[::2].contiguous(), p)
+    torch.cuda.synchronize()
+    assert all(torch.equal(a, b) for a, b in zip(ref, got))
+    rs = gpu.phg.trace_device_rows(f, sp[::2], sd[::2], p)
+    o2, v2, e2 = rs.to_csr()
+    assert torch.equal(o2, ref[0]) and torch.equal(v2, ref[1])
+    with pytest.raises(DataError):
+        gpu.phg.trace_device(f, sp.float(), sd.float(), p)
+    with pytest.raises(DataError):
+        gpu.phg.trace_device_rows(f, sp, sd[:10], p)

@@ -122,3 +122,26 @@ def test_default_trace_kernels_do_not_spill():
             assert "LOCAL:0" in res and "STACK:0" in res, (ln, res)
             assert reg <= 128, (ln, res)  # 4 CTAs of 128 threads per SM
     assert seen >= 12, seen
+
+
+def test_round2_entry_points_validate_without_gpu(lib):
+    """The round-2 entry points reject bad arguments with PHG_ERR_INVALID (no CUDA call is
+    made), and the release build says it is not the checked build."""
+    from paper_2604_05794_b200 import _native
+
+    INV, STATE = _native.PHG_ERR_INVALID, _native.PHG_ERR_STATE
+    rows = _native.Rows()
+    assert lib.phg_trace_rows(None, None, None, None, None, 0, ctypes.byref(rows), None) == INV
+    assert lib.phg_gather_to(None, None, None, None, 0, 0, None) == INV
+    assert lib.phg_ipc_open(None, ctypes.byref(ctypes.c_void_p())) == INV
+    assert lib.phg_ipc_alloc(-1, ctypes.byref(ctypes.c_void_p()), None) == INV
+    origin = (ctypes.c_double * 3)(0, 0, 0)
+    assert lib.phg_field_create_packed(None, 4, 4, 4, origin, 1.0, 1, 1.0, None) == INV
+    out = ctypes.c_void_p()
+    assert lib.phg_field_create_packed(ctypes.byref(out), 0, 4, 4, origin, 1.0, 1, 1.0,
+                                       None) == INV
+    assert lib.phg_field_packed(None, None, None, None, None) == INV
+    assert lib.phg_field_packed_done(None, None) == INV
+    assert lib.phg_is_checked_build() == 0
+    v = ctypes.c_int64()
+    assert lib.phg_debug_checks(ctypes.byref(v), None, None) == STATE
