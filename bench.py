@@ -575,6 +575,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     rows_steps = rs.steps
     accepted = tracer.last_steps()
+    kernel_variant = {"variant": tracer.last_variant(), "sampler": tracer.last_sampler()}
     del rs
     if rows_steps != my_steps:
         raise RuntimeError(f"rows path steps {rows_steps} != CSR path steps {my_steps}")
@@ -667,6 +668,7 @@ def run_ours(args):
                       ":keep[i]], phg.py:159-162); value_csr adds the CSR scan + gather (K2)",
             "value_csr": value_csr, "ms_per_step_csr": ms_csr,
             "roofline": roofline_block(cfg, accepted, kernel_ms),
+            "trace_kernel": kernel_variant,
             "cpu_baseline": cpu, "e2e": e2e, "clocks": clk, "driver": driver, "a9": a9,
             "dropin": dropin, "setup": setup, "root_gather": root_gather,
             "gpu_launches": args.steps * phg.LAUNCHES_PER_TRACE_ROWS,

@@ -41,16 +41,18 @@ def _compile(args):
     return src, r
 
 
-def build(force=False, verbose=False, checked=False):
+def build(force=False, verbose=False, checked=False, extra=(), out=None):
     """checked=True: libphg_b200_checked.so with -DPHG_CHECKED (device index checks and
     allocation canaries; loaded with PHG_CHECKED_LIB=1).  The translation units compile in
-    parallel (one nvcc per file), then link into the shared library."""
-    out = OUT_CHECKED if checked else OUT
+    parallel (one nvcc per file), then link into the shared library.  `extra` nvcc flags and
+    another `out` path build experiment libraries for A/B runs (loaded with PHG_LIB_PATH)."""
+    out = out or (OUT_CHECKED if checked else OUT)
     deps = SRCS + HDRS + [os.path.join(ROOT, "include", "phg_b200.h")]
     if (not force and os.path.exists(out)
             and os.path.getmtime(out) >= max(os.path.getmtime(d) for d in deps)):
         return out
-    flags = NVCC_FLAGS + (["-DPHG_CHECKED"] if checked else [])
+    flags = NVCC_FLAGS + (["-DPHG_CHECKED"] if checked else []) + list(extra)
+    os.makedirs(os.path.dirname(os.path.abspath(out)), exist_ok=True)
     objdir = tempfile.mkdtemp(prefix="phg_build_")
     try:
         jobs = [(src, os.path.join(objdir, os.path.basename(src) + ".o"), flags) for src in SRCS]

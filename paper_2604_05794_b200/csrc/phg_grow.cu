@@ -296,7 +296,7 @@ __global__ void unvisited_flag_kernel(FieldView F, const uint32_t* __restrict__ 
                                       long long nvox, uint8_t* __restrict__ flag) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nvox;
          i += (long long)gridDim.x * blockDim.x)
-        flag[i] = (F.vox[vox_index_lin(F, (uint32_t)i)].w != 0.0f && (counts[i] & 0xffffu) == 0u)
+        flag[i] = (occ_live(F.vox[vox_index_lin(F, (uint32_t)i)].w) && (counts[i] & 0xffffu) == 0u)
                       ? 1
                       : 0;
 }

@@ -160,7 +160,7 @@ phg_status phg_field_from_oovl(phg_field** out, const uint8_t* bits, const float
         delete f;
         return fail(PHG_ERR_CUDA, "oovl_scatter_kernel: %s", cudaGetErrorString(e));
     }
-    s = field_build_bricks(f, st);
+    s = field_finish(f, st);
     if (s != PHG_OK) {
         delete f;
         return s;

@@ -182,7 +182,13 @@ def test_every_kernel_variant_bit_exact(gpu, oracle_c, monkeypatch):
     cap = np.random.Generator(np.random.Philox(key=5)).random(vol.occ.shape) < 0.02
     tracer = gpu.phg._tracer()
     names, samplers = [], set()
-    for v in range(_native.load().phg_num_variants()):
+    nv = _native.load().phg_num_variants()
+    for v in range(nv):
+        # variant 0 (block signs) needs a field with block bounds, the last variant (bare
+        # occupancy flags) one without: forced here, as this sparse field would pick the latter
+        if v in (0, nv - 1):
+            monkeypatch.setenv("PHG_BLOCK_SIGN", "1" if v == 0 else "0")
+            gpu.volume.invalidate()
         monkeypatch.setenv("PHG_VARIANT", str(v))
         for plane in (None, cap):
             _compare_with_oracle(gpu, oracle_c, vol, s, d, p, at_cap=plane)
@@ -190,6 +196,115 @@ def test_every_kernel_variant_bit_exact(gpu, oracle_c, monkeypatch):
         samplers.add(tracer.last_sampler())
     assert len(set(names)) == len(names), names
     assert samplers == {"exact", "fast-pow2"}, samplers
+    gpu.volume.invalidate()
+
+
+def _packed_block_bounds(gpu, f, dims):
+    """(occupancy flags, block bound floats) of a device field's padded voxels."""
+    torch = gpu.torch
+    ptr, nbytes, zeroed, _ = f.packed()
+    assert zeroed
+    arr = gpu.phg._CudaArray(ptr, (nbytes // 4,), "<u4")
+    w = torch.as_tensor(arr, device="cuda").view(-1, 4)[:, 3].cpu().numpy()
+    nx, ny, nz = dims
+    w = w.reshape(nx + 2, ny + 2, nz + 2)
+    live = (w & np.uint32(0xFFF00000)) == np.uint32(0x3FF00000)
+    dead_ok = (w & np.uint32(0xFFF00000)) == 0
+    assert np.all(live | dead_ok)
+    t = ((w & np.uint32(0xFFFFF)) << np.uint32(12)).view(np.float32)
+    return live, t
+
+
+@pytest.mark.parametrize("kind,fill", [("curly", None), ("sparse", None), ("fuzz", 0.5)])
+def test_block_bounds_cover_corner_spread(gpu, monkeypatch, kind, fill):
+    """The packed field's block bounds (csrc/phg_core.cuh block_bound): for every block with
+    an occupied base, t >= max over the occupied corners of |o_k - o_base|_1 (computed here
+    in exact fp64); -inf exactly for blocks with no occupied corner; +inf for an unoccupied
+    base with an occupied corner.  These bounds are what lets one fp32 dot decide all eight
+    corner signs, so an undershoot would be a parity bug."""
+    if kind == "fuzz":
+        rng = np.random.default_rng(7)
+        dims = (23, 17, 29)
+        occ, ori = _fuzz_field(rng, dims, fill, False)
+    else:
+        from paper_2604_05794_b200 import synth
+
+        ori, occ = synth.make_field(kind, 48, "cpu")
+        ori, occ = ori.numpy(), occ.numpy()
+        dims = occ.shape
+    monkeypatch.setenv("PHG_BLOCK_SIGN", "0")  # no bounds: .w is the bare occupancy flag
+    f = gpu.volume.DeviceField(np.zeros(3), 2.0, occ, ori)
+    try:
+        live, t = _packed_block_bounds(gpu, f, dims)
+    finally:
+        f.close()
+    assert np.all(t == 0)
+    monkeypatch.setenv("PHG_BLOCK_SIGN", "1")  # bounds written whatever the field's sparsity
+    f = gpu.volume.DeviceField(np.zeros(3), 2.0, occ, ori)
+    try:
+        live, t = _packed_block_bounds(gpu, f, dims)
+    finally:
+        f.close()
+    nx, ny, nz = dims
+    po = np.zeros((nx + 2, ny + 2, nz + 2), bool)
+    po[1:-1, 1:-1, 1:-1] = occ
+    pv = np.zeros((nx + 2, ny + 2, nz + 2, 3), np.float64)
+    pv[1:-1, 1:-1, 1:-1] = np.where(occ[..., None], ori, 0.0)
+    assert np.array_equal(live, po)
+    base_o, base_v = po[:-1, :-1, :-1], pv[:-1, :-1, :-1]
+    spread = np.zeros(base_o.shape)
+    anylive = np.zeros(base_o.shape, bool)
+    for k in range(1, 8):
+        dx, dy, dz = k >> 2, (k >> 1) & 1, k & 1
+        ok = po[dx:dx + nx + 1, dy:dy + ny + 1, dz:dz + nz + 1]
+        ov = pv[dx:dx + nx + 1, dy:dy + ny + 1, dz:dz + nz + 1]
+        sk = np.abs(ov - base_v).sum(-1)
+        spread = np.where(ok, np.maximum(spread, sk), spread)
+        anylive |= ok
+    tb = t[:-1, :-1, :-1].astype(np.float64)
+    assert np.all(tb[base_o] >= spread[base_o]), float((spread - tb)[base_o].max())
+    assert np.all(np.isneginf(tb[~base_o & ~anylive]))
+    assert np.all(np.isposinf(tb[~base_o & anylive]))
+    assert np.all(np.isposinf(t[-1, :, :])) and np.all(np.isposinf(t[:, -1, :]))
+
+
+@pytest.mark.parametrize("kind,interior", [("curly", 0), ("sparse", 1_500), ("fuzz", 0)])
+def test_block_signs_forced_on_and_off_bit_exact(gpu, oracle_c, monkeypatch, kind, interior):
+    """The trace kernel with one fp32 dot per certified corner block (Cfg::BSIGN) and with
+    per-corner dots only, each forced on both a dense and a sparse field (the automatic
+    choice takes the first on C3-like fields, the second on C5-like ones), equal the oracle
+    bit for bit, with and without a cap plane."""
+    if kind == "fuzz":
+        rng = np.random.default_rng(11)
+        dims = (31, 26, 35)
+        occ, ori = _fuzz_field(rng, dims, 0.85, False)
+        vol = SimpleNamespace(origin=np.zeros(3), voxel_size=2.0, dims=dims, occ=occ, ori=ori)
+        s = _fuzz_points(rng, dims, 2.0, 4_000)[8:]
+        d = rng.normal(size=s.shape)
+        p = SimpleNamespace(step_mm=1.0, max_vertices=200, min_support=0.05, probe_steps=24,
+                            coast_steps=25, steer=0.0, strict=False)
+    else:
+        vol, s, d, p = _config_case(kind, 48, 3_000, 61, interior=interior)
+    cap = np.random.default_rng(3).random(vol.occ.shape) < 0.02
+    tr = gpu.phg._tracer()
+    try:
+        for force in ("1", "0", None):
+            if force is None:
+                monkeypatch.delenv("PHG_BLOCK_SIGN", raising=False)
+            else:
+                monkeypatch.setenv("PHG_BLOCK_SIGN", force)
+            gpu.volume.invalidate()
+            # the angle-stop kernel always has the block test compiled in: on a field without
+            # bounds it must fall through to the per-corner dots
+            turn = SimpleNamespace(**vars(p), max_turn_deg=8.0)
+            _compare_with_oracle(gpu, oracle_c, vol, s, d, turn, at_cap=cap)
+            for plane in (None, cap):
+                _compare_with_oracle(gpu, oracle_c, vol, s, d, p, at_cap=plane)
+            on = tr.last_variant().endswith("+bsign")
+            want = force == "1" if force is not None else {"curly": True, "sparse": False}.get(kind)
+            assert want is None or on == want, (force, kind, tr.last_variant())
+    finally:
+        gpu.volume.invalidate()
 
 
 @pytest.mark.parametrize("kind,vs,nan,want", [
