@@ -3,7 +3,7 @@
 # registers / spills and the opcode histogram.  Usage: sass_stats.sh <lib.so> <mangled-suffix>
 # e.g. the C3 default kernel: Li0ELb0ELi2ELb0ELb0E (CAP none, no steering, fast pow2 sampler)
 set -eu
-lib=$(realpath "$1"); pat=${2:-Li0ELb0ELi2ELb0ELb0E}; cfg=${CFG:-ILi1ELi1ELi4ELi8ELi128ELb1ELi4ELb1ELb1EEE}
+lib=$(realpath "$1"); pat=${2:-Li0ELb0ELi2ELb0ELb0E}; cfg=${CFG:-ILi1ELi1ELi4ELi8ELi128ELb1ELi4ELb1ELi1EEE}
 d=$(mktemp -d); trap 'rm -rf $d' EXIT
 (cd $d && cuobjdump -xelf phg_trace.sm_100a.cubin "$lib" >/dev/null)
 nvdisasm -c $d/phg_trace.sm_100a.cubin > $d/all.sass

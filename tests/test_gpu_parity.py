@@ -217,11 +217,11 @@ def _packed_block_bounds(gpu, f, dims):
 
 @pytest.mark.parametrize("kind,fill", [("curly", None), ("sparse", None), ("fuzz", 0.5)])
 def test_block_bounds_cover_corner_spread(gpu, monkeypatch, kind, fill):
-    """The packed field's block bounds (csrc/phg_core.cuh block_bound): for every block with
-    an occupied base, t >= max over the occupied corners of |o_k - o_base|_1 (computed here
-    in exact fp64); -inf exactly for blocks with no occupied corner; +inf for an unoccupied
-    base with an occupied corner.  These bounds are what lets one fp32 dot decide all eight
-    corner signs, so an undershoot would be a parity bug."""
+    """The packed field's block bounds (csrc/phg_core.cuh block_bound): for every fully
+    occupied block, t >= max over its corners of |o_k - o_base|_1 (computed here in exact
+    fp64); +inf for every other block.  These bounds are what lets one fp32 dot decide all
+    eight corner signs (and skip the occupancy tests), so an undershoot would be a parity
+    bug."""
     if kind == "fuzz":
         rng = np.random.default_rng(7)
         dims = (23, 17, 29)
@@ -251,20 +251,19 @@ def test_block_bounds_cover_corner_spread(gpu, monkeypatch, kind, fill):
     pv = np.zeros((nx + 2, ny + 2, nz + 2, 3), np.float64)
     pv[1:-1, 1:-1, 1:-1] = np.where(occ[..., None], ori, 0.0)
     assert np.array_equal(live, po)
-    base_o, base_v = po[:-1, :-1, :-1], pv[:-1, :-1, :-1]
-    spread = np.zeros(base_o.shape)
-    anylive = np.zeros(base_o.shape, bool)
-    for k in range(1, 8):
+    base_v = pv[:-1, :-1, :-1]
+    spread = np.zeros(base_v.shape[:3])
+    full = np.ones(base_v.shape[:3], bool)
+    for k in range(8):
         dx, dy, dz = k >> 2, (k >> 1) & 1, k & 1
-        ok = po[dx:dx + nx + 1, dy:dy + ny + 1, dz:dz + nz + 1]
+        full &= po[dx:dx + nx + 1, dy:dy + ny + 1, dz:dz + nz + 1]
         ov = pv[dx:dx + nx + 1, dy:dy + ny + 1, dz:dz + nz + 1]
-        sk = np.abs(ov - base_v).sum(-1)
-        spread = np.where(ok, np.maximum(spread, sk), spread)
-        anylive |= ok
+        spread = np.maximum(spread, np.abs(ov - base_v).sum(-1))
     tb = t[:-1, :-1, :-1].astype(np.float64)
-    assert np.all(tb[base_o] >= spread[base_o]), float((spread - tb)[base_o].max())
-    assert np.all(np.isneginf(tb[~base_o & ~anylive]))
-    assert np.all(np.isposinf(tb[~base_o & anylive]))
+    assert full.any()
+    assert np.all(np.isfinite(tb[full]))
+    assert np.all(tb[full] >= spread[full]), float((spread - tb)[full].max())
+    assert np.all(np.isposinf(tb[~full]))
     assert np.all(np.isposinf(t[-1, :, :])) and np.all(np.isposinf(t[:, -1, :]))
 
 
