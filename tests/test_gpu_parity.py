@@ -211,7 +211,8 @@ def _packed_block_bounds(gpu, f, dims):
     live = (w & np.uint32(0xFFF00000)) == np.uint32(0x3FF00000)
     dead_ok = (w & np.uint32(0xFFF00000)) == 0
     assert np.all(live | dead_ok)
-    t = ((w & np.uint32(0xFFFFF)) << np.uint32(12)).view(np.float32)
+    # the top 20 bits of a double's high word (low word 0)
+    t = ((w & np.uint32(0xFFFFF)).astype(np.uint64) << np.uint64(44)).view(np.float64)
     return live, t
 
 
@@ -259,7 +260,7 @@ def test_block_bounds_cover_corner_spread(gpu, monkeypatch, kind, fill):
         full &= po[dx:dx + nx + 1, dy:dy + ny + 1, dz:dz + nz + 1]
         ov = pv[dx:dx + nx + 1, dy:dy + ny + 1, dz:dz + nz + 1]
         spread = np.maximum(spread, np.abs(ov - base_v).sum(-1))
-    tb = t[:-1, :-1, :-1].astype(np.float64)
+    tb = t[:-1, :-1, :-1]
     assert full.any()
     assert np.all(np.isfinite(tb[full]))
     assert np.all(tb[full] >= spread[full]), float((spread - tb)[full].max())
