@@ -87,7 +87,10 @@ phg_status phg_field_info(const phg_field* f, int64_t dims[3], int* device);
  * phg_field_packed: the padded packed voxel buffer (device pointer, bytes) and its flags.
  * phg_field_create_packed: a field of the given geometry whose packed buffer the caller then
  *   fills (e.g. the NCCL broadcast of another rank's phg_field_packed buffer), followed by
- *   phg_field_packed_done (derived structures, e.g. the optional bricked copy). */
+ *   phg_field_packed_done (derived structures: the block sign bounds in the voxels' low .w
+ *   bits, recomputed from the buffer, and the optional bricked copy).  The buffer format is
+ *   this library build's own; it is meant for replication between ranks running the same
+ *   build. */
 phg_status phg_field_packed(const phg_field* f, void** vox, int64_t* bytes, int32_t* zeroed,
                             float* maxabs);
 phg_status phg_field_create_packed(phg_field** out, int64_t nx, int64_t ny, int64_t nz,
