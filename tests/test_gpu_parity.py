@@ -912,3 +912,26 @@ def test_device_api_validates_and_copies_strided_seeds(gpu):
         gpu.phg.trace_device(f, sp.float(), sd.float(), p)
     with pytest.raises(DataError):
         gpu.phg.trace_device_rows(f, sp, sd[:10], p)
+
+
+@pytest.mark.parametrize("kind", ["straight", "curly"])
+def test_certified_blocks_against_the_field_bit_exact(gpu, oracle_c, kind):
+    """Strands running against the field direction on a dense field: every certified block has
+    the negative sign, so the unsigned block sums are flipped (0 + s*sum).  The straight field's
+    x/y sums are exactly zero, which exercises the sign-of-zero argument of that flip.  Seeds
+    start mid-height, with exact and tilted directions, plus exactly orthogonal ones (d0 = 0:
+    never certified)."""
+    vol, _, _, p = _config_case(kind, 40, 10, 71)
+    rng = np.random.default_rng(71)
+    n = 3000
+    L = 40 * synth_voxel()
+    r = 0.4 * L * np.sqrt(rng.random(n))
+    th = 2 * np.pi * rng.random(n)
+    s = np.stack([L / 2 + r * np.cos(th), L / 2 + r * np.sin(th), rng.uniform(0.3, 0.7, n) * L], 1)
+    d = np.tile([0.0, 0.0, -1.0], (n, 1))
+    d[n // 3: 2 * n // 3] += rng.normal(scale=0.2, size=(n // 3, 3))
+    d[2 * n // 3:] = np.stack([np.cos(th[2 * n // 3:]), np.sin(th[2 * n // 3:]),
+                               np.zeros(n - 2 * n // 3)], 1)
+    gpu.volume.invalidate()
+    _compare_with_oracle(gpu, oracle_c, vol, s, d, p)
+    assert gpu.phg._tracer().last_variant().endswith("+bsign")
