@@ -937,3 +937,24 @@ def test_certified_blocks_against_the_field_bit_exact(gpu, oracle_c, kind):
     gpu.volume.invalidate()
     _compare_with_oracle(gpu, oracle_c, vol, s, d, p)
     assert gpu.phg._tracer().last_variant().endswith("+bsign")
+
+
+@pytest.mark.parametrize("scale", [1e3, 1.0, 1e-20, 1e-30])
+def test_block_signs_on_scaled_and_noisy_fields_bit_exact(gpu, oracle_c, monkeypatch, scale):
+    """Block sign certificates (forced on) on a dense field whose orientations are scaled far
+    from unit length and carry per-voxel noise, so the bounds, sign_eps and the base dot all
+    scale together and a share of the blocks fails the certificate: equal to the oracle."""
+    vol, s, d, p = _config_case("curly", 32, 4_000, 83)
+    rng = np.random.default_rng(83)
+    noise = rng.normal(scale=0.05, size=vol.ori.shape).astype(np.float32)
+    vol.ori = np.where(vol.occ[..., None], (vol.ori + noise) * np.float32(scale), 0.0)
+    vol.ori = vol.ori.astype(np.float32)
+    d = d + rng.normal(scale=0.3, size=d.shape)
+    monkeypatch.setenv("PHG_BLOCK_SIGN", "1")
+    gpu.volume.invalidate()
+    try:
+        for cap in (None, rng.random(vol.occ.shape) < 0.03):
+            _compare_with_oracle(gpu, oracle_c, vol, s, d, p, at_cap=cap)
+        assert gpu.phg._tracer().last_variant().endswith("+bsign")
+    finally:
+        gpu.volume.invalidate()
